@@ -1,0 +1,375 @@
+"""Benchmark: MoE-layer tokens/s/GPU + scheduler µs/iter (Qwen3-MoE shape) on B200.
+
+Contract (see task spec): one JSON line on rank 0.
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--tokens T] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "c2"): Qwen3-30B-A3B-shaped MoE layer —
+128 experts, top-8, d_h=2048, d_e=768, SwiGLU, bf16 random-init weights, the
+committed c2 replica map (N=1, reference placement pipeline), Zipf(1.0)
+routing from gen_batch (seed 0x30).  One step = one MoE layer over one batch of
+T tokens: K1 schedule + K3 permute + K4 grouped GEMMs + K5 combine.  The
+weight store (1.21 GB) is far larger than L2, so every step streams it from HBM.
+
+Under torchrun (N > 1) every rank runs the same single-GPU layer on its own
+batch ("replicas", weak scaling) — the attention->MoE split lives in
+paper_2512_13525_b200/dist.py and bench_dist.py.
+
+``--impl reference`` times the reference's CPU path on the host cores: the
+reference's own schedule() (oracle/_ref, compiled from /root/reference) plus
+the oracle's fp32 SwiGLU expert FFN (the reference has no FFN), on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+E, K_TOP, D_H, D_E = 128, 8, 2048, 768
+SEED = 0x30
+MAP = "c2"
+N_BATCHES = 8  # distinct routing batches rotated through the timed steps
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.05)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_sample(T, tokens_sample, batches, layer_experts_w, nthreads):
+    """Time the reference CPU path on a bounded sample: reference schedule() on
+    the full batch + oracle fp32 SwiGLU FFN for `tokens_sample` tokens' rows."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import CSRMap, Oracle, Ref
+
+    import paper_2512_13525_b200 as J
+    ref, orc = Ref(), Oracle()
+    rm = J.config_map(MAP)
+    m = CSRMap(rm.num_experts, rm.num_instances, rm.slots_per_instance, *rm.csr())
+    b0 = batches[0]
+    t_sched = ref.time_schedule(np.concatenate(batches), T, K_TOP, m, "schedule", reps=21) * 1e-6
+    t_sched_ref = ref.time_schedule(np.concatenate(batches), T, K_TOP, m, "reference",
+                                    reps=21) * 1e-6
+    ex = b0.reshape(T, K_TOP)[:tokens_sample]
+    by_e = {}
+    for t in range(tokens_sample):
+        for j in range(K_TOP):
+            by_e.setdefault(int(ex[t, j]), []).append(t)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((tokens_sample, D_H)).astype(np.float32)
+    xu = orc.f32_to_bf16(x)
+    ws_ = {e: layer_experts_w(e) for e in by_e}  # weight generation outside the timing
+    t0 = time.perf_counter()
+    for e, toks in by_e.items():
+        wg, wu, wd = ws_[e]
+        orc.expert_swiglu(xu[toks], wg, wu, wd, round_h=True, nthreads=nthreads)
+    t_ffn = time.perf_counter() - t0
+    t_step_sample = t_ffn + t_sched * tokens_sample / T
+    return {"tok_s": tokens_sample / t_step_sample, "t_sched_us": t_sched * 1e6,
+            "t_sched_reference_us": t_sched_ref * 1e6, "t_ffn_s": t_ffn,
+            "sample_tokens": tokens_sample}
+
+
+def cpu_weights_fn():
+    """Deterministic CPU-side bf16 expert weights for the CPU sample (the CPU
+    arm has no GPU; numbers only need the right shape)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle
+    orc = Oracle()
+    cache = {}
+
+    def fn(e):
+        if e not in cache:
+            r = np.random.default_rng(e)
+            cache[e] = tuple(orc.f32_to_bf16(r.standard_normal(s).astype(np.float32) * sc)
+                             for s, sc in (((D_E, D_H), D_H ** -0.5), ((D_E, D_H), D_H ** -0.5),
+                                           ((D_H, D_E), D_E ** -0.5)))
+        return cache[e]
+    return fn
+
+
+def gen_batches(T):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import paper_2512_13525_b200 as J
+    pat = J.RoutingPattern.zipf(E, 1.0)
+    return [J.gen_batch(pat, T, K_TOP, SEED, T * 1000 + i).experts for i in range(N_BATCHES)]
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    T = args.tokens
+    batches = gen_batches(T)
+    nthreads = os.cpu_count() or 1
+    wfn = cpu_weights_fn()
+    sample = max(1, min(T, args.cpu_sample_tokens))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(T, sample, batches, wfn, nthreads)
+        if i >= args.warmup:
+            vals.append(r)
+    tok_s = float(np.median([v["tok_s"] for v in vals]))
+    line = {
+        "impl": "reference", "metric": "moe_layer_tokens_per_s_per_gpu", "value": tok_s,
+        "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic", "config": workload_config(T, args),
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": nthreads,
+                         "kind": "reference",
+                         "sample": f"reference schedule() (oracle/_ref, 4-thread OMP team as "
+                                   f"shipped) on the full T={T} batch, pro-rated, + fp32 SwiGLU "
+                                   f"FFN (oracle port; reference has none) for {sample} tokens "
+                                   f"x top-8 rows on {nthreads} threads"},
+        "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "scheduler": {"cpu_schedule_us": float(np.median([v["t_sched_us"] for v in vals])),
+                      "cpu_schedule_reference_us": float(np.median(
+                          [v["t_sched_reference_us"] for v in vals]))},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(T, args):
+    return {"workload": "c2: Qwen3-30B-A3B-shaped MoE layer (128 experts, top-8, d_h=2048, "
+                        "d_e=768, SwiGLU) on 1 B200 per rank: AEBS scheduler + grouped FFN",
+            "tokens_per_step": T, "experts": E, "top_k": K_TOP, "d_hidden": D_H,
+            "d_expert": D_E, "routing": "Zipf s=1.0 via gen_batch, seed 0x30",
+            "replica_map": "maps/c2.map (reference placement pipeline)",
+            "l2": "inputs > L2: 1.21 GB expert weights streamed from HBM every step",
+            "parallelism": f"replicas x{args.gpus}"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_13525_b200 as J
+    from paper_2512_13525_b200._lib import lib
+    from paper_2512_13525_b200.moe import MoELayer, build_weight_store, make_inputs
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    T = args.tokens
+
+    rmap = J.config_map(MAP)
+    layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=-1, device=local)
+    w13, w2 = build_weight_store(layer, seed=1)
+    layer.set_weights(w13, w2)
+    batches = [torch.from_numpy(b).to(dev) for b in gen_batches(T)]
+    x, gw = make_inputs(T, K_TOP, D_H, 3, dev)
+    out = torch.empty_like(x)
+
+    # algorithmic bytes / flops of the grouped GEMMs for each batch
+    sched = layer.sched
+    alg_bytes, alg_flops = [], []
+    for b in gen_batches(T):
+        a = sched.schedule(J.ActivationBatch(T, K_TOP, b))
+        A = int((a.expert_instance >= 0).sum())
+        rows = T * K_TOP
+        alg_bytes.append(A * 3 * D_H * D_E * 2 + rows * (D_H + D_E) * 2 * 2)
+        alg_flops.append(6.0 * D_H * D_E * rows)
+
+    def step(i):
+        layer.forward(x, batches[i % N_BATCHES], gw, out=out)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches0 = layer.launches()
+    lib.janus_profile(layer.ctx, 1)
+    s = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(s)
+        for i in range(args.steps):
+            step(i)
+        e1.record(s)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = layer.launches() - launches0
+    import ctypes as C
+    sched_ms, ffn_ms, calls = C.c_double(), C.c_double(), C.c_int()
+    lib.janus_profile_read(layer.ctx, C.byref(sched_ms), C.byref(ffn_ms), C.byref(calls))
+    lib.janus_profile(layer.ctx, 0)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = T * args.steps * ws / (ms / 1e3)
+
+    # e2e through the public host API: pinned host buffers, H2D + layer + D2H each step
+    xh = x.cpu().pin_memory()
+    gh = gw.cpu().pin_memory()
+    bh = [b.cpu().pin_memory() for b in batches]
+    oh = torch.empty(T, D_H, dtype=torch.bfloat16).pin_memory()
+    for i in range(max(1, args.warmup)):
+        layer.forward_host(xh, bh[i % N_BATCHES], gh, oh)
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        layer.forward_host(xh, bh[i % N_BATCHES], gh, oh)
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = T * args.steps * ws / e2e_s
+
+    # scheduler µs/iter (graph-replayed) on the same batch
+    sched_us = sched.time_schedule(batches[0], T, K_TOP, reps=51)
+
+    hbm, tf_burst, tf_sus, src = peaks()
+    ffn_s = ffn_ms.value / 1e3 / max(calls.value, 1)
+    bytes_avg = float(np.mean([alg_bytes[i % N_BATCHES] for i in range(args.steps)]))
+    flops_avg = float(np.mean([alg_flops[i % N_BATCHES] for i in range(args.steps)]))
+    gbs = bytes_avg / ffn_s / 1e9
+    tfs = flops_avg / ffn_s / 1e12
+    hbm_bound = gbs / hbm >= tfs / (tf_sus or tf_burst)
+    roofline = ({"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                 "traffic": None} if hbm_bound else
+                {"bound": "tensor", "achieved": tfs, "peak": tf_sus or tf_burst,
+                 "unit": "TFLOP/s", "frac": tfs / (tf_sus or tf_burst), "traffic": None})
+    roofline.update({"kernel": "grouped_gemm_kernel (gate-up SwiGLU + down), per layer call",
+                     "peak_source": f"{src} (MEASURED_PEAKS.json)",
+                     "ffn_us_per_step": ffn_s * 1e6,
+                     "ffn_share_of_step": ffn_s * 1e3 / ms_per_step,
+                     "alg_bytes_per_step": bytes_avg, "alg_flops_per_step": flops_avg,
+                     "hbm_frac": gbs / hbm, "tensor_frac": tfs / (tf_sus or tf_burst)})
+    if rank != 0:
+        dist.destroy_process_group() if ws > 1 else None
+        return
+
+    cpu = None
+    if not args.no_cpu:
+        try:
+            r = cpu_sample(T, max(1, min(T, args.cpu_sample_tokens)), gen_batches(T),
+                           cpu_weights_fn(), os.cpu_count() or 1)
+            cpu = {"value": r["tok_s"], "unit": "tokens/s", "cores": os.cpu_count() or 1,
+                   "kind": "reference",
+                   "sample": f"reference schedule() (oracle/_ref) on the full batch, pro-rated, "
+                             f"+ oracle fp32 SwiGLU FFN for {r['sample_tokens']} tokens "
+                             f"(x top-8 rows); reference schedule() {r['t_sched_us']:.1f} us, "
+                             f"schedule_reference() {r['t_sched_reference_us']:.1f} us"}
+            cpu_sched = (r["t_sched_us"], r["t_sched_reference_us"])
+        except Exception as ex:  # oracle/_ref missing on this box
+            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+            cpu_sched = (None, None)
+    else:
+        cpu_sched = (None, None)
+
+    line = {
+        "metric": "moe_layer_tokens_per_s_per_gpu", "value": value, "unit": "tokens/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (gen_batch Zipf routing, random-init bf16 weights)",
+        "config": workload_config(T, args),
+        "tokens_per_s_per_gpu": value / ws,
+        "scheduler": {"us_per_iter": sched_us, "how": "CUDA-graph replay of 20 passes, median",
+                      "cpu_schedule_us": cpu_sched[0], "cpu_schedule_reference_us": cpu_sched[1]},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "tokens/s",
+                "h2d_bytes_per_step": T * D_H * 2 + T * K_TOP * 8,
+                "d2h_bytes_per_step": T * D_H * 2},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--tokens", type=int, default=4096)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-tokens", type=int, default=16)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * janus_b200.h — C ABI of the B200-native MoE-side hot path of Janus
+ * (arXiv 2512.13525): activation-balanced expert scheduling (AEBS), the
+ * dispatch layout, the per-GPU SwiGLU expert FFN, combine, and the
+ * attention->MoE / MoE->attention exchange inside one NVLink box.
+ *
+ * Plain C types only (no torch types).  Entry points marked "device" take
+ * device pointers and are stream-ordered and asynchronous (no host sync);
+ * entry points marked "host" take host buffers and synchronise.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   janus_set_replica_map  <- ReplicaMap + ReplicaMap::validate
+ *                             (include/moesim/aebs.hpp:29-38, src/aebs.cpp:49-77)
+ *   janus_schedule[_async] <- moesim::schedule / schedule_reference /
+ *                             schedule_random (include/moesim/aebs.hpp:63-71,
+ *                             src/aebs.cpp:172-262) returning Assignment
+ *                             (aebs.hpp:42-50)
+ *   janus_moe_layer[_async]<- moe_layer_latency's subject: the MoE layer the
+ *                             reference only models (src/latency.cpp:17-32)
+ *   janus_moe_layer_latency<- moesim::moe_layer_latency (latency.hpp:34-35)
+ *   janus_gen_batch        <- moesim::gen_batch (include/moesim/workload.hpp:31-32)
+ *   janus_shard_tokens     <- StepTraffic token ownership (src/comm.cpp:76-81)
+ * See INTEGRATION.md for the binding a maintainer adds on the reference side.
+ */
+#ifndef JANUS_B200_H_
+#define JANUS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  JANUS_OK = 0,
+  JANUS_EINVAL = 1,          /* ValidationError-class input problem (types.hpp:20-22) */
+  JANUS_EUNKNOWN_EXPERT = 2, /* aebs.cpp:22-25 "unknown-expert: ..." */
+  JANUS_ECUDA = 3,           /* CUDA runtime/driver failure */
+  JANUS_ESTATE = 4,          /* call order: no map / no weights / not reserved */
+  JANUS_EUNSUPPORTED = 5     /* shape outside this build's kernel limits */
+} janus_status;
+
+typedef enum {
+  JANUS_POLICY_AEBS = 0,   /* schedule() == schedule_reference() outputs */
+  JANUS_POLICY_RANDOM = 1  /* schedule_random(seed) */
+} janus_policy;
+
+/* Kernel limits of this build. */
+#define JANUS_MAX_EXPERTS 1024
+#define JANUS_MAX_INSTANCES 1024
+#define JANUS_MAX_REPLICAS 8192
+
+typedef struct janus_ctx janus_ctx;
+
+/* One scheduling pass, device side.  Every pointer is a caller-owned device
+ * buffer.  The first five are the reference Assignment (aebs.hpp:42-50); the
+ * rest are the dispatch layout and may be NULL.
+ * status[0] receives JANUS_OK / JANUS_EUNKNOWN_EXPERT, status[1] the bad
+ * expert id (the minimum one, as schedule() reports it, aebs.cpp:137-162). */
+typedef struct {
+  int32_t *instance;        /* [T*k]  instance of each token slot            */
+  int32_t *replica;         /* [T*k]  physical replica id of each slot       */
+  int32_t *expert_instance; /* [E]    -1 when inactive                       */
+  int32_t *load;            /* [N]    activated replicas hosted              */
+  int64_t *routed_tokens;   /* [N]    token activations routed               */
+  int64_t *expert_tokens;   /* [E]    token activations per expert (opt)     */
+  int32_t *slot_row;        /* [T*k]  row of each slot in the dispatch layout */
+  int32_t *row_slot;        /* [T*k]  inverse permutation                    */
+  int32_t *group_off;       /* [R+1]  row offset of each replica group       */
+  int32_t *status;          /* [2]    {status, bad expert}                   */
+} janus_assignment;
+
+/* ---- context ------------------------------------------------------------ */
+janus_status janus_create(janus_ctx **ctx, int device);
+void janus_destroy(janus_ctx *ctx);
+/* Last error message of this context, in the reference's wording. */
+const char *janus_last_error(const janus_ctx *ctx);
+/* Number of kernels this context has launched (instrumentation). */
+uint64_t janus_launch_count(const janus_ctx *ctx);
+
+/* ---- replica map (host) ------------------------------------------------- */
+/* CSR: hosts[off[e]..off[e+1]) strictly ascending instance ids of expert e,
+ * rid[] parallel opaque physical replica ids.  Validated as
+ * ReplicaMap::validate (aebs.cpp:49-77), then uploaded once. */
+janus_status janus_set_replica_map(janus_ctx *ctx, int num_experts, int num_instances,
+                                   int slots_per_instance, const int32_t *off,
+                                   const int32_t *hosts, const int32_t *rid);
+/* Replica order used by the dispatch layout and the weight store: for each
+ * CSR entry p, qidx[p] = flat index of that replica (instance-major, ordered
+ * by (replica id, expert) within an instance); qbase[g] = first index of
+ * instance g (N+1 entries).  Host buffers. */
+janus_status janus_replica_order(const janus_ctx *ctx, int32_t *qidx, int32_t *qbase);
+
+/* ---- scheduler ---------------------------------------------------------- */
+/* device: one fused kernel (K1+K2), stream-ordered, no host sync. */
+janus_status janus_schedule_async(janus_ctx *ctx, const int32_t *d_experts, int num_tokens,
+                                  int top_k, int policy, uint64_t seed,
+                                  const janus_assignment *out, void *stream);
+/* host: the drop-in for moesim::schedule()/schedule_random().  Host buffers,
+ * synchronous.  Returns JANUS_EUNKNOWN_EXPERT with janus_last_error() set to
+ * the reference message.  expert_tokens may be NULL. */
+janus_status janus_schedule(janus_ctx *ctx, const int32_t *experts, int num_tokens, int top_k,
+                            int policy, uint64_t seed, int32_t *instance, int32_t *replica,
+                            int32_t *expert_instance, int32_t *load, int64_t *routed_tokens,
+                            int64_t *expert_tokens);
+/* Median device time (µs, CUDA events, graph-replayed) of `reps` scheduler
+ * passes over a device-resident batch. */
+janus_status janus_time_schedule(janus_ctx *ctx, const int32_t *d_experts, int num_tokens,
+                                 int top_k, int policy, int reps, double *median_us);
+
+/* ---- MoE layer ---------------------------------------------------------- */
+/* Expert FFN shape (SwiGLU, bf16 weights, fp32 accumulate) and the largest
+ * step this context must hold (allocates workspace). */
+janus_status janus_moe_configure(janus_ctx *ctx, int d_hidden, int d_expert, int max_tokens,
+                                 int top_k);
+/* Weight store of the local instance `instance` (or -1: this GPU holds every
+ * instance's replicas): device bf16 buffers in replica order (qidx, qbase)
+ *   w13: [Q][2*d_expert][d_hidden]  rows 0..d_e-1 gate, d_e..2d_e-1 up
+ *   w2 : [Q][d_hidden][d_expert]    down projection
+ * Q = replicas hosted (qbase[g+1]-qbase[g], or R).  Not copied: must outlive
+ * the context. */
+janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *d_w13,
+                                   const void *d_w2);
+/* device: K1 schedule -> K3 permute -> K4 grouped SwiGLU GEMMs -> K5 combine.
+ *   x [T][d_h] bf16, experts [T*k] int32, gate_w [T*k] fp32, out [T][d_h] bf16.
+ * With a single-instance weight store (instance >= 0) out receives this
+ * instance's partial sum (tokens routed elsewhere contribute 0).
+ * If `assign` is non-NULL the scheduling outputs are also written there. */
+janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
+                                   const float *d_gate_w, int num_tokens, void *d_out,
+                                   const janus_assignment *assign, void *stream);
+/* host: end to end from (pinned) host buffers: H2D, layer, D2H, sync. */
+janus_status janus_moe_layer(janus_ctx *ctx, const void *x, const int32_t *experts,
+                             const float *gate_w, int num_tokens, void *out);
+
+/* ---- instrumentation ---------------------------------------------------- */
+/* While enabled, every janus_moe_layer_async call records CUDA events on its
+ * stream around the scheduler kernel (K1+K2) and around the grouped GEMMs (K4).
+ * janus_profile_read synchronises, returns the summed device times (ms) and
+ * the number of layer calls recorded, and resets. */
+janus_status janus_profile(janus_ctx *ctx, int enable);
+janus_status janus_profile_read(janus_ctx *ctx, double *sched_ms, double *ffn_ms, int *calls);
+
+/* ---- attention <-> MoE exchange (one NVLink box) ------------------------ */
+/* Token ownership on the attention side: even split, remainder to the lowest
+ * ids (comm.cpp:76-81).  Writes first token and count of shard a. */
+void janus_shard_tokens(int64_t num_tokens, int attn_instances, int a, int64_t *first,
+                        int64_t *count);
+
+/* ---- model / workload --------------------------------------------------- */
+/* The reference roofline prediction (latency.cpp:17-32), kept for comparison
+ * with measured layer times. */
+double janus_moe_layer_latency(int num_instances, const int32_t *load,
+                               const int64_t *routed_tokens, int d_hidden, int d_expert,
+                               int bytes_per_param, double peak_flops, double hbm_bandwidth,
+                               double t_launch);
+/* Synthetic routing exactly as gen_batch (workload.cpp:56-130) from an
+ * inclusive cdf of num_experts doubles (RoutingPattern::cdf). */
+janus_status janus_gen_batch(const double *cdf, int num_experts, int num_tokens, int top_k,
+                             uint64_t seed, uint64_t step, int32_t *out);
+uint64_t janus_derive_seed(uint64_t root, const char *label, uint64_t extra);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JANUS_B200_H_ */

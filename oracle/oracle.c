@@ -577,9 +577,13 @@ void or_expert_swiglu(const uint16_t *x, int n, const uint16_t *wg, const uint16
   float *wgf = (float *)malloc(sizeof(float) * (size_t)d_e * d_h);
   float *wuf = (float *)malloc(sizeof(float) * (size_t)d_e * d_h);
   float *wdf = (float *)malloc(sizeof(float) * (size_t)d_h * d_e);
-  or_bf16_to_f32(wg, wgf, (long long)d_e * d_h);
-  or_bf16_to_f32(wu, wuf, (long long)d_e * d_h);
-  or_bf16_to_f32(wd, wdf, (long long)d_h * d_e);
+  const long long nw = (long long)d_e * d_h;
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+  for (long long i = 0; i < nw; ++i) {
+    wgf[i] = bf16_to_f32(wg[i]);
+    wuf[i] = bf16_to_f32(wu[i]);
+    wdf[i] = bf16_to_f32(wd[i]);
+  }
 #pragma omp parallel for schedule(dynamic) num_threads(nthreads > 0 ? nthreads : 1)
   for (int r = 0; r < n; ++r) {
     float *xf = (float *)malloc(sizeof(float) * d_h);

@@ -1,0 +1,72 @@
+"""ctypes binding of libjanus_b200.so (the C ABI in include/janus_b200.h).
+
+The library is built in-tree by ``paper_2512_13525_b200/build.py`` (or
+``__graft_entry__.build()``).  There is no fallback: if the library is missing,
+importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libjanus_b200.so")
+
+OK, EINVAL, EUNKNOWN_EXPERT, ECUDA, ESTATE, EUNSUPPORTED = range(6)
+POLICY_AEBS, POLICY_RANDOM = 0, 1
+STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "EUNKNOWN_EXPERT", 3: "ECUDA", 4: "ESTATE",
+                5: "EUNSUPPORTED"}
+
+# Every entry point include/janus_b200.h declares (checked by tests/test_abi.py).
+SYMBOLS = (
+    "janus_create", "janus_destroy", "janus_last_error", "janus_launch_count",
+    "janus_set_replica_map", "janus_replica_order", "janus_schedule_async", "janus_schedule",
+    "janus_time_schedule", "janus_moe_configure", "janus_moe_set_weights",
+    "janus_moe_layer_async", "janus_moe_layer", "janus_shard_tokens",
+    "janus_moe_layer_latency", "janus_gen_batch", "janus_derive_seed", "janus_profile",
+    "janus_profile_read",
+)
+
+
+class JanusAssignment(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in (
+        "instance", "replica", "expert_instance", "load", "routed_tokens", "expert_tokens",
+        "slot_row", "row_slot", "group_off", "status")]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, u64, dbl = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double
+    P = C.POINTER
+    L.janus_create.argtypes = [P(vp), i32]
+    L.janus_destroy.argtypes = [vp]
+    L.janus_destroy.restype = None
+    L.janus_last_error.argtypes = [vp]
+    L.janus_last_error.restype = C.c_char_p
+    L.janus_launch_count.argtypes = [vp]
+    L.janus_launch_count.restype = u64
+    L.janus_set_replica_map.argtypes = [vp, i32, i32, i32, vp, vp, vp]
+    L.janus_replica_order.argtypes = [vp, vp, vp]
+    L.janus_schedule_async.argtypes = [vp, vp, i32, i32, i32, u64, P(JanusAssignment), vp]
+    L.janus_schedule.argtypes = [vp, vp, i32, i32, i32, u64, vp, vp, vp, vp, vp, vp]
+    L.janus_time_schedule.argtypes = [vp, vp, i32, i32, i32, i32, P(dbl)]
+    L.janus_moe_configure.argtypes = [vp, i32, i32, i32, i32]
+    L.janus_moe_set_weights.argtypes = [vp, i32, vp, vp]
+    L.janus_moe_layer_async.argtypes = [vp, vp, vp, vp, i32, vp, P(JanusAssignment), vp]
+    L.janus_moe_layer.argtypes = [vp, vp, vp, vp, i32, vp]
+    L.janus_shard_tokens.argtypes = [i64, i32, i32, P(i64), P(i64)]
+    L.janus_shard_tokens.restype = None
+    L.janus_moe_layer_latency.argtypes = [i32, vp, vp, i32, i32, i32, dbl, dbl, dbl]
+    L.janus_moe_layer_latency.restype = dbl
+    L.janus_gen_batch.argtypes = [vp, i32, i32, i32, u64, u64, vp]
+    L.janus_derive_seed.argtypes = [u64, C.c_char_p, u64]
+    L.janus_derive_seed.restype = u64
+    L.janus_profile.argtypes = [vp, i32]
+    L.janus_profile_read.argtypes = [vp, P(dbl), P(dbl), P(i32)]
+    return L
+
+
+lib = _load()

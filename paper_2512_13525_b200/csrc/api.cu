@@ -1,0 +1,572 @@
+// api.cu — the C ABI (include/janus_b200.h): context, replica-map upload and
+// validation, scheduling, MoE layer orchestration.  Host code only; kernels
+// live in aebs.cu / ffn.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using janus::DevMap;
+
+namespace {
+
+janus_status fail(janus_ctx *c, janus_status st, const std::string &msg) {
+  if (c) c->err = msg;
+  return st;
+}
+
+janus_status cuda_fail(janus_ctx *c, cudaError_t e, const char *where) {
+  return fail(c, JANUS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                        \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call); \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t n) {
+  return cudaMalloc(reinterpret_cast<void **>(p), std::max<size_t>(n, 1) * sizeof(T));
+}
+
+void dfree(void *p) {
+  if (p) cudaFree(p);
+}
+
+void free_map(DevMap &m) {
+  dfree(m.off);
+  dfree(m.hosts);
+  dfree(m.rid);
+  dfree(m.qidx);
+  dfree(m.hmask);
+  m = DevMap{};
+}
+
+void free_assign(janus_assignment &a) {
+  dfree(a.instance);
+  dfree(a.replica);
+  dfree(a.expert_instance);
+  dfree(a.load);
+  dfree(a.routed_tokens);
+  dfree(a.expert_tokens);
+  dfree(a.slot_row);
+  dfree(a.row_slot);
+  dfree(a.group_off);
+  dfree(a.status);
+  a = janus_assignment{};
+}
+
+cudaError_t alloc_assign(janus_assignment &a, int S, int E, int N, int R) {
+  cudaError_t e;
+  if ((e = dalloc(&a.instance, S)) || (e = dalloc(&a.replica, S)) ||
+      (e = dalloc(&a.expert_instance, E)) || (e = dalloc(&a.load, N)) ||
+      (e = dalloc(&a.routed_tokens, N)) || (e = dalloc(&a.expert_tokens, E)) ||
+      (e = dalloc(&a.slot_row, S)) || (e = dalloc(&a.row_slot, S)) ||
+      (e = dalloc(&a.group_off, R + 1)) || (e = dalloc(&a.status, 2)))
+    return e;
+  return cudaSuccess;
+}
+
+// --- rng (include/moesim/rng.hpp:13-44), used for schedule_random seeds and
+// the synthetic workload generator.
+uint64_t splitmix64(uint64_t &s) {
+  s += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t hash_label(const char *label) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (const unsigned char *p = reinterpret_cast<const unsigned char *>(label); *p; ++p) {
+    h ^= *p;
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+janus_status check_ready(janus_ctx *ctx) {
+  if (!ctx) return JANUS_EINVAL;
+  if (!ctx->have_map) return fail(ctx, JANUS_ESTATE, "janus: no replica map set");
+  return JANUS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t janus_derive_seed(uint64_t root, const char *label, uint64_t extra) {
+  uint64_t s = root;
+  splitmix64(s);
+  s ^= hash_label(label);
+  splitmix64(s);
+  uint64_t e = extra;
+  s ^= splitmix64(e);
+  return splitmix64(s);
+}
+
+janus_status janus_create(janus_ctx **out, int device) {
+  if (!out) return JANUS_EINVAL;
+  *out = nullptr;
+  janus_ctx *ctx = new janus_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return JANUS_ECUDA;
+  }
+  *out = ctx;
+  return JANUS_OK;
+}
+
+void janus_destroy(janus_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  free_map(ctx->dmap);
+  dfree(ctx->d_in);
+  free_assign(ctx->d_out);
+  free_assign(ctx->ws);
+  dfree(ctx->ws_tile_off);
+  dfree(ctx->ffn.xp);
+  dfree(ctx->ffn.h);
+  dfree(ctx->ffn.y);
+  dfree(ctx->d_x);
+  dfree(ctx->d_outbuf);
+  dfree(ctx->d_experts);
+  dfree(ctx->d_gw);
+  for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char *janus_last_error(const janus_ctx *ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+uint64_t janus_launch_count(const janus_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+// ReplicaMap::validate, src/aebs.cpp:49-77 (same messages).
+janus_status janus_set_replica_map(janus_ctx *ctx, int E, int N, int C, const int32_t *off,
+                                   const int32_t *hosts, const int32_t *rid) {
+  if (!ctx) return JANUS_EINVAL;
+  if (E <= 0 || N <= 0 || C <= 0)
+    return fail(ctx, JANUS_EINVAL, "replica map: dimensions must be positive");
+  if (!off || !hosts || !rid || off[0] != 0)
+    return fail(ctx, JANUS_EINVAL, "replica map: per-expert tables sized wrong");
+  std::vector<int> used(N, 0);
+  for (int e = 0; e < E; ++e) {
+    if (off[e + 1] <= off[e])
+      return fail(ctx, JANUS_EINVAL,
+                  "replica map: expert " + std::to_string(e) + " has no replica");
+    for (int i = off[e]; i < off[e + 1]; ++i) {
+      const int g = hosts[i];
+      if (g < 0 || g >= N)
+        return fail(ctx, JANUS_EINVAL,
+                    "replica map: expert " + std::to_string(e) + " hosted on invalid instance " +
+                        std::to_string(g));
+      if (i > off[e] && hosts[i - 1] >= g)
+        return fail(ctx, JANUS_EINVAL,
+                    "replica map: expert " + std::to_string(e) +
+                        " host list not strictly ascending");
+      ++used[g];
+    }
+  }
+  for (int g = 0; g < N; ++g)
+    if (used[g] > C)
+      return fail(ctx, JANUS_EINVAL,
+                  "replica map: instance " + std::to_string(g) + " holds " +
+                      std::to_string(used[g]) + " replicas, capacity " + std::to_string(C));
+  const int R = off[E];
+  if (E > JANUS_MAX_EXPERTS || N > JANUS_MAX_INSTANCES || R > JANUS_MAX_REPLICAS ||
+      janus::schedule_smem_bytes(E, N, R) > 227 * 1024 - 1024)
+    return fail(ctx, JANUS_EUNSUPPORTED, "replica map: exceeds kernel limits of this build");
+
+  ctx->off.assign(off, off + E + 1);
+  ctx->hosts.assign(hosts, hosts + R);
+  ctx->rid.assign(rid, rid + R);
+  // Replica order: per instance, sorted by (replica id, expert).
+  std::vector<int32_t> expert_of(R);
+  for (int e = 0; e < E; ++e)
+    for (int p = off[e]; p < off[e + 1]; ++p) expert_of[p] = e;
+  std::vector<int> order(R);
+  for (int p = 0; p < R; ++p) order[p] = p;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    if (hosts[a] != hosts[b]) return hosts[a] < hosts[b];
+    if (rid[a] != rid[b]) return rid[a] < rid[b];
+    return expert_of[a] < expert_of[b];
+  });
+  ctx->qidx.assign(R, 0);
+  ctx->qbase.assign(N + 1, 0);
+  for (int i = 0; i < R; ++i) {
+    ctx->qidx[order[i]] = i;
+    ctx->qbase[hosts[order[i]] + 1]++;
+  }
+  for (int g = 0; g < N; ++g) ctx->qbase[g + 1] += ctx->qbase[g];
+  std::vector<uint32_t> hm(E, 0);
+  if (N <= 32)
+    for (int e = 0; e < E; ++e)
+      for (int p = off[e]; p < off[e + 1]; ++p) hm[e] |= 1u << hosts[p];
+
+  CK(cudaSetDevice(ctx->device));
+  free_map(ctx->dmap);
+  DevMap &m = ctx->dmap;
+  CK(dalloc(&m.off, E + 1));
+  CK(dalloc(&m.hosts, R));
+  CK(dalloc(&m.rid, R));
+  CK(dalloc(&m.qidx, R));
+  CK(dalloc(&m.hmask, E));
+  CK(cudaMemcpy(m.off, off, sizeof(int32_t) * (E + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.hosts, hosts, sizeof(int32_t) * R, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.rid, rid, sizeof(int32_t) * R, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.qidx, ctx->qidx.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m.hmask, hm.data(), sizeof(uint32_t) * E, cudaMemcpyHostToDevice));
+  m.E = E;
+  m.N = N;
+  m.C = C;
+  m.R = R;
+  ctx->have_map = true;
+  // a new map invalidates the layer's weight store
+  ctx->moe_ready = false;
+  ctx->ffn.w13 = ctx->ffn.w2 = nullptr;
+  return JANUS_OK;
+}
+
+janus_status janus_replica_order(const janus_ctx *ctx, int32_t *qidx, int32_t *qbase) {
+  if (!ctx || !ctx->have_map) return JANUS_ESTATE;
+  std::copy(ctx->qidx.begin(), ctx->qidx.end(), qidx);
+  std::copy(ctx->qbase.begin(), ctx->qbase.end(), qbase);
+  return JANUS_OK;
+}
+
+static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T, int k,
+                                 int policy, uint64_t seed, const janus_assignment &out,
+                                 int32_t *tile_off, cudaStream_t stream) {
+  if (T < 0 || k <= 0 || (int64_t)T * k > (int64_t)1 << 30)
+    return fail(ctx, JANUS_EINVAL, "batch: num_tokens must be >= 0 and top_k >= 1");
+  if (policy != JANUS_POLICY_AEBS && policy != JANUS_POLICY_RANDOM)
+    return fail(ctx, JANUS_EINVAL, "schedule: unknown policy");
+  if (!out.instance || !out.replica || !out.expert_instance || !out.load || !out.routed_tokens ||
+      !out.status || (T > 0 && !d_experts))
+    return fail(ctx, JANUS_EINVAL, "schedule: missing output buffer");
+  janus::SchedArgs a{};
+  a.experts = d_experts;
+  a.S = T * k;
+  a.k = k;
+  a.map = ctx->dmap;
+  a.policy = policy;
+  a.rng_state = janus_derive_seed(seed, "sched/random", 0);
+  a.out = out;
+  a.tile_off = tile_off;
+  cudaError_t e = janus::launch_schedule(a, stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "aebs_schedule_kernel");
+  ctx->launches += 1;
+  return JANUS_OK;
+}
+
+janus_status janus_schedule_async(janus_ctx *ctx, const int32_t *d_experts, int T, int k,
+                                  int policy, uint64_t seed, const janus_assignment *out,
+                                  void *stream) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (!out) return fail(ctx, JANUS_EINVAL, "schedule: null output");
+  return launch_sched(ctx, d_experts, T, k, policy, seed, *out, nullptr,
+                      static_cast<cudaStream_t>(stream));
+}
+
+static janus_status grow_sched(janus_ctx *ctx, int S) {
+  if (S <= ctx->sched_cap && ctx->d_in) return JANUS_OK;
+  const int cap = std::max(S, 1024);
+  dfree(ctx->d_in);
+  free_assign(ctx->d_out);
+  ctx->d_in = nullptr;
+  CK(dalloc(&ctx->d_in, cap));
+  CK(alloc_assign(ctx->d_out, cap, JANUS_MAX_EXPERTS, JANUS_MAX_INSTANCES,
+                  JANUS_MAX_REPLICAS));
+  ctx->sched_cap = cap;
+  return JANUS_OK;
+}
+
+janus_status janus_schedule(janus_ctx *ctx, const int32_t *experts, int T, int k, int policy,
+                            uint64_t seed, int32_t *instance, int32_t *replica,
+                            int32_t *expert_instance, int32_t *load, int64_t *routed_tokens,
+                            int64_t *expert_tokens) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (T < 0 || k <= 0) return fail(ctx, JANUS_EINVAL, "batch: num_tokens must be >= 0 and top_k >= 1");
+  CK(cudaSetDevice(ctx->device));
+  const int S = T * k;
+  st = grow_sched(ctx, S);
+  if (st != JANUS_OK) return st;
+  cudaStream_t s = ctx->stream;
+  if (S) CK(cudaMemcpyAsync(ctx->d_in, experts, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s));
+  st = launch_sched(ctx, ctx->d_in, T, k, policy, seed, ctx->d_out, nullptr, s);
+  if (st != JANUS_OK) return st;
+  int32_t status[2];
+  CK(cudaMemcpyAsync(status, ctx->d_out.status, sizeof(status), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (status[0] == JANUS_EUNKNOWN_EXPERT)
+    return fail(ctx, JANUS_EUNKNOWN_EXPERT,
+                "unknown-expert: batch references expert " + std::to_string(status[1]) +
+                    " with no replica in the map");
+  const DevMap &m = ctx->dmap;
+  if (S) {
+    CK(cudaMemcpyAsync(instance, ctx->d_out.instance, sizeof(int32_t) * S,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(replica, ctx->d_out.replica, sizeof(int32_t) * S, cudaMemcpyDeviceToHost,
+                       s));
+  }
+  CK(cudaMemcpyAsync(expert_instance, ctx->d_out.expert_instance, sizeof(int32_t) * m.E,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(load, ctx->d_out.load, sizeof(int32_t) * m.N, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(routed_tokens, ctx->d_out.routed_tokens, sizeof(int64_t) * m.N,
+                     cudaMemcpyDeviceToHost, s));
+  if (expert_tokens)
+    CK(cudaMemcpyAsync(expert_tokens, ctx->d_out.expert_tokens, sizeof(int64_t) * m.E,
+                       cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return JANUS_OK;
+}
+
+janus_status janus_time_schedule(janus_ctx *ctx, const int32_t *d_experts, int T, int k,
+                                 int policy, int reps, double *median_us) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  CK(cudaSetDevice(ctx->device));
+  st = grow_sched(ctx, T * k);
+  if (st != JANUS_OK) return st;
+  cudaStream_t s = ctx->stream;
+  constexpr int kPerGraph = 20;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < kPerGraph; ++i) {
+    st = launch_sched(ctx, d_experts, T, k, policy, 1, ctx->d_out, nullptr, s);
+    if (st != JANUS_OK) {
+      cudaStreamEndCapture(s, &graph);
+      return st;
+    }
+  }
+  CK(cudaStreamEndCapture(s, &graph));
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (int i = 0; i < 3; ++i) CK(cudaGraphLaunch(exec, s));
+  std::vector<float> t(std::max(reps, 1));
+  for (auto &x : t) {
+    CK(cudaEventRecord(e0, s));
+    CK(cudaGraphLaunch(exec, s));
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&x, e0, e1));
+  }
+  ctx->launches += (uint64_t)kPerGraph * (t.size() + 3);
+  std::nth_element(t.begin(), t.begin() + t.size() / 2, t.end());
+  *median_us = 1000.0 * t[t.size() / 2] / kPerGraph;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  return JANUS_OK;
+}
+
+// ---------------------------------------------------------------- MoE -----
+
+janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_tokens, int k) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (d_h <= 0 || d_e <= 0 || d_h % 256 || d_e % 128 || max_tokens <= 0 || k <= 0)
+    return fail(ctx, JANUS_EUNSUPPORTED,
+                "moe: need d_hidden % 256 == 0, d_expert % 128 == 0, max_tokens, top_k > 0");
+  CK(cudaSetDevice(ctx->device));
+  const int S = max_tokens * k;
+  const int S_alloc = S + janus::kTileN;  // tail room for the last token box
+  dfree(ctx->ffn.xp);
+  dfree(ctx->ffn.h);
+  dfree(ctx->ffn.y);
+  free_assign(ctx->ws);
+  dfree(ctx->ws_tile_off);
+  dfree(ctx->d_x);
+  dfree(ctx->d_outbuf);
+  dfree(ctx->d_experts);
+  dfree(ctx->d_gw);
+  ctx->ffn.xp = ctx->ffn.h = ctx->ffn.y = nullptr;
+  ctx->ws_tile_off = nullptr;
+  ctx->d_x = ctx->d_outbuf = nullptr;
+  ctx->d_experts = nullptr;
+  ctx->d_gw = nullptr;
+  const DevMap &m = ctx->dmap;
+  CK(cudaMalloc(&ctx->ffn.xp, (size_t)S_alloc * d_h * 2));
+  CK(cudaMalloc(&ctx->ffn.h, (size_t)S_alloc * d_e * 2));
+  CK(cudaMalloc(&ctx->ffn.y, (size_t)S_alloc * d_h * 2));
+  CK(cudaMemset(ctx->ffn.xp, 0, (size_t)S_alloc * d_h * 2));
+  CK(cudaMemset(ctx->ffn.h, 0, (size_t)S_alloc * d_e * 2));
+  CK(alloc_assign(ctx->ws, S, m.E, m.N, m.R));
+  CK(dalloc(&ctx->ws_tile_off, m.R + 1));
+  CK(cudaMalloc(&ctx->d_x, (size_t)max_tokens * d_h * 2));
+  CK(cudaMalloc(&ctx->d_outbuf, (size_t)max_tokens * d_h * 2));
+  CK(dalloc(&ctx->d_experts, S));
+  CK(dalloc(&ctx->d_gw, S));
+  ctx->d_h = d_h;
+  ctx->d_e = d_e;
+  ctx->max_tokens = max_tokens;
+  ctx->top_k = k;
+  ctx->ffn.d_h = d_h;
+  ctx->ffn.d_e = d_e;
+  ctx->ffn.S_alloc = S_alloc;
+  ctx->moe_ready = false;
+  return JANUS_OK;
+}
+
+janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *w13, const void *w2) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (!ctx->ffn.xp) return fail(ctx, JANUS_ESTATE, "moe: janus_moe_configure first");
+  if (!w13 || !w2 || instance >= ctx->dmap.N)
+    return fail(ctx, JANUS_EINVAL, "moe: bad weight store");
+  CK(cudaSetDevice(ctx->device));
+  ctx->instance = instance;
+  ctx->ffn.q_begin = instance < 0 ? 0 : ctx->qbase[instance];
+  ctx->ffn.q_end = instance < 0 ? ctx->dmap.R : ctx->qbase[instance + 1];
+  ctx->ffn.w13 = w13;
+  ctx->ffn.w2 = w2;
+  CK(janus::build_ffn_tensor_maps(ctx->ffn));
+  ctx->moe_ready = true;
+  return JANUS_OK;
+}
+
+janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
+                                   const float *d_gate_w, int T, void *d_out,
+                                   const janus_assignment *assign, void *stream) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (!ctx->moe_ready) return fail(ctx, JANUS_ESTATE, "moe: weights not set");
+  if (T < 0 || T > ctx->max_tokens)
+    return fail(ctx, JANUS_EINVAL, "moe: num_tokens outside [0, max_tokens]");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int k = ctx->top_k;
+  janus_assignment a = ctx->ws;
+  if (assign) {  // caller wants the scheduling outputs: write into its buffers
+    a.instance = assign->instance ? assign->instance : a.instance;
+    a.replica = assign->replica ? assign->replica : a.replica;
+    a.expert_instance = assign->expert_instance ? assign->expert_instance : a.expert_instance;
+    a.load = assign->load ? assign->load : a.load;
+    a.routed_tokens = assign->routed_tokens ? assign->routed_tokens : a.routed_tokens;
+    a.expert_tokens = assign->expert_tokens ? assign->expert_tokens : a.expert_tokens;
+    a.slot_row = assign->slot_row ? assign->slot_row : a.slot_row;
+    a.row_slot = assign->row_slot ? assign->row_slot : a.row_slot;
+    a.group_off = assign->group_off ? assign->group_off : a.group_off;
+    a.status = assign->status ? assign->status : a.status;
+  }
+  cudaEvent_t *ev = nullptr;
+  if (ctx->profiling) {
+    const size_t need = 4 * (size_t)(ctx->prof_calls + 1);
+    while (ctx->prof_events.size() < need) {
+      cudaEvent_t x;
+      CK(cudaEventCreate(&x));
+      ctx->prof_events.push_back(x);
+    }
+    ev = &ctx->prof_events[4 * (size_t)ctx->prof_calls];
+    ctx->prof_calls++;
+    CK(cudaEventRecord(ev[0], s));
+  }
+  st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, ctx->ws_tile_off, s);
+  if (st != JANUS_OK) return st;
+  if (ev) CK(cudaEventRecord(ev[1], s));
+  janus::FfnPlan &p = ctx->ffn;
+  cudaError_t e =
+      janus::launch_permute(d_x, a.row_slot, a.group_off, p.q_begin, p.q_end, k, p.d_h, p.xp, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "permute_kernel");
+  int launches = 0;
+  if (ev) CK(cudaEventRecord(ev[2], s));
+  e = janus::launch_ffn(p, a.group_off, ctx->ws_tile_off, s, &launches);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "grouped_gemm_kernel");
+  if (ev) CK(cudaEventRecord(ev[3], s));
+  e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
+                            d_out, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
+  ctx->launches += 2 + launches;
+  return JANUS_OK;
+}
+
+janus_status janus_moe_layer(janus_ctx *ctx, const void *x, const int32_t *experts,
+                             const float *gate_w, int T, void *out) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (!ctx->moe_ready) return fail(ctx, JANUS_ESTATE, "moe: weights not set");
+  if (T < 0 || T > ctx->max_tokens)
+    return fail(ctx, JANUS_EINVAL, "moe: num_tokens outside [0, max_tokens]");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const size_t S = (size_t)T * ctx->top_k;
+  CK(cudaMemcpyAsync(ctx->d_x, x, (size_t)T * ctx->d_h * 2, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_experts, experts, S * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_gw, gate_w, S * 4, cudaMemcpyHostToDevice, s));
+  st = janus_moe_layer_async(ctx, ctx->d_x, ctx->d_experts, ctx->d_gw, T, ctx->d_outbuf, nullptr,
+                             s);
+  if (st != JANUS_OK) return st;
+  int32_t status[2];
+  CK(cudaMemcpyAsync(out, ctx->d_outbuf, (size_t)T * ctx->d_h * 2, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(status, ctx->ws.status, sizeof(status), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (status[0] == JANUS_EUNKNOWN_EXPERT)
+    return fail(ctx, JANUS_EUNKNOWN_EXPERT,
+                "unknown-expert: batch references expert " + std::to_string(status[1]) +
+                    " with no replica in the map");
+  return JANUS_OK;
+}
+
+janus_status janus_profile(janus_ctx *ctx, int enable) {
+  if (!ctx) return JANUS_EINVAL;
+  ctx->profiling = enable != 0;
+  ctx->prof_calls = 0;
+  return JANUS_OK;
+}
+
+janus_status janus_profile_read(janus_ctx *ctx, double *sched_ms, double *ffn_ms, int *calls) {
+  if (!ctx) return JANUS_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  double a = 0, b = 0;
+  for (int i = 0; i < ctx->prof_calls; ++i) {
+    cudaEvent_t *ev = &ctx->prof_events[4 * (size_t)i];
+    float x = 0, y = 0;
+    CK(cudaEventSynchronize(ev[3]));
+    CK(cudaEventElapsedTime(&x, ev[0], ev[1]));
+    CK(cudaEventElapsedTime(&y, ev[2], ev[3]));
+    a += x;
+    b += y;
+  }
+  if (sched_ms) *sched_ms = a;
+  if (ffn_ms) *ffn_ms = b;
+  if (calls) *calls = ctx->prof_calls;
+  ctx->prof_calls = 0;
+  return JANUS_OK;
+}
+
+void janus_shard_tokens(int64_t T, int A, int a, int64_t *first, int64_t *count) {
+  // src/comm.cpp:76-81: even split, remainder to the lowest instance ids
+  const int64_t base = T / A, rem = T % A;
+  *count = base + (a < rem ? 1 : 0);
+  *first = a * base + std::min<int64_t>(a, rem);
+}
+
+// src/latency.cpp:17-32 (the reference's accounting, unchanged).
+double janus_moe_layer_latency(int N, const int32_t *load, const int64_t *routed, int d_h,
+                               int d_e, int bpp, double peak_flops, double hbm_bw,
+                               double t_launch) {
+  double worst = 0;
+  for (int g = 0; g < N; ++g) {
+    if (load[g] <= 0) continue;
+    const double mem = load[g] * (2.0 * d_h * d_e * bpp) / hbm_bw;
+    const double comp = 2.0 * static_cast<double>(routed[g]) * d_h * d_e / peak_flops;
+    worst = std::max(worst, t_launch + std::max(mem, comp));
+  }
+  return worst;
+}
+
+}  // extern "C"

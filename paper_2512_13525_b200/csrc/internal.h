@@ -1,0 +1,94 @@
+// internal.h — context and shared declarations of libjanus_b200.so.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "janus_b200.h"
+
+namespace janus {
+
+constexpr int kSchedThreads = 1024;  // one CTA, 32 warps
+
+// Map-derived tables on the device (uploaded once per janus_set_replica_map).
+struct DevMap {
+  int E = 0, N = 0, C = 0, R = 0;
+  int32_t *off = nullptr, *hosts = nullptr, *rid = nullptr, *qidx = nullptr;
+  uint32_t *hmask = nullptr;  // per-expert host bitmask (N <= 32 only)
+};
+
+struct SchedArgs {
+  const int32_t *experts;
+  int S, k;
+  DevMap map;
+  int policy;
+  uint64_t rng_state;  // derive_seed(seed, "sched/random")
+  janus_assignment out;
+  int32_t *tile_off;   // [R+1] n-tile prefix for the grouped GEMM (BN = kTileN), optional
+};
+
+// Launches the fused scheduler + layout kernel (aebs.cu).
+cudaError_t launch_schedule(const SchedArgs &a, cudaStream_t stream);
+size_t schedule_smem_bytes(int E, int N, int R);
+
+// MoE FFN workspace (ffn.cu).
+constexpr int kTileN = 128;  // token rows per GEMM tile (UMMA N <= 128)
+
+struct FfnPlan {
+  int d_h = 0, d_e = 0, S_alloc = 0;
+  int q_begin = 0, q_end = 0;   // replica groups computed here
+  const void *w13 = nullptr, *w2 = nullptr;
+  void *xp = nullptr, *h = nullptr, *y = nullptr;  // bf16 [S_alloc][.]
+  CUtensorMap tm_w13, tm_w2;
+  CUtensorMap tm_xp[4], tm_h[4];  // box rows 16/32/64/128
+  bool maps_ready = false;
+};
+
+cudaError_t build_ffn_tensor_maps(FfnPlan &p);
+cudaError_t launch_permute(const void *x, const int32_t *row_slot, const int32_t *group_off,
+                           int q_begin, int q_end, int k, int d_h, void *xp, cudaStream_t s);
+cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
+                       cudaStream_t s, int *launches);
+cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
+                           int instance, const float *gate_w, int T, int k, int d_h, void *out,
+                           cudaStream_t s);
+
+}  // namespace janus
+
+struct janus_ctx {
+  int device = 0;
+  std::string err;
+  uint64_t launches = 0;
+  cudaStream_t stream = nullptr;  // internal stream for host-API calls
+
+  // replica map (host copies + device tables)
+  bool have_map = false;
+  std::vector<int32_t> off, hosts, rid, qidx, qbase;
+  janus::DevMap dmap;
+
+  // scratch for the host scheduling API (grown on demand)
+  int sched_cap = 0;
+  int32_t *d_in = nullptr;
+  janus_assignment d_out{};
+  int32_t *d_status = nullptr;
+
+  // MoE layer
+  bool moe_ready = false;
+  int d_h = 0, d_e = 0, max_tokens = 0, top_k = 0, instance = -1;
+  janus::FfnPlan ffn;
+  janus_assignment ws{};      // device workspace for the layer's assignment
+  int32_t *ws_tile_off = nullptr;
+  // staging for the host MoE API
+  void *d_x = nullptr, *d_outbuf = nullptr;
+  int32_t *d_experts = nullptr;
+  float *d_gw = nullptr;
+
+  // instrumentation (janus_profile)
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_events;  // 4 per recorded call
+  int prof_calls = 0;
+};

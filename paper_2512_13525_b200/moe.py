@@ -1,0 +1,140 @@
+"""The MoE layer on one GPU: K1 schedule -> K3 permute -> K4 grouped SwiGLU GEMMs
+-> K5 combine, all in libjanus_b200.so.  torch is used only for device memory
+and streams.
+
+Weight store: replicas in the replica order the dispatch layout uses
+(``Scheduler.replica_order``): for the replicas hosted on an instance, sorted
+by (replica id, expert).  ``w13[q] = [Wg; Wu]`` (2*d_e x d_h), ``w2[q] = Wd``
+(d_h x d_e), bf16.  A replica holds its logical expert's weights.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from ._lib import OK, EUNKNOWN_EXPERT, JanusAssignment, lib
+from .moesim import JanusError, ReplicaMap, Scheduler, ValidationError, derive_seed
+
+
+def _cur_stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class MoELayer:
+    def __init__(self, rmap: ReplicaMap, d_hidden: int, d_expert: int, max_tokens: int,
+                 top_k: int, instance: int = -1, device: int = 0):
+        self.sched = Scheduler(rmap, device)
+        self.map = rmap
+        self.d_h, self.d_e, self.k = d_hidden, d_expert, top_k
+        self.max_tokens = max_tokens
+        self.instance = instance
+        self.device = torch.device("cuda", device)
+        st = lib.janus_moe_configure(self.ctx, d_hidden, d_expert, max_tokens, top_k)
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+        self.qidx, self.qbase = self.sched.replica_order()
+        off, _, _ = self.sched._csr
+        # expert held at each replica-order index q
+        self.q_expert = np.zeros(int(off[-1]), np.int32)
+        for e in range(rmap.num_experts):
+            for p in range(off[e], off[e + 1]):
+                self.q_expert[self.qidx[p]] = e
+        self.w13 = self.w2 = None
+
+    @property
+    def ctx(self):
+        return self.sched.ctx
+
+    def local_experts(self) -> np.ndarray:
+        """Logical expert of each local weight slot (replica order)."""
+        if self.instance < 0:
+            return self.q_expert.copy()
+        return self.q_expert[self.qbase[self.instance]:self.qbase[self.instance + 1]].copy()
+
+    def set_weights(self, w13: torch.Tensor, w2: torch.Tensor) -> None:
+        Q = len(self.local_experts())
+        assert w13.shape == (Q, 2 * self.d_e, self.d_h) and w13.dtype == torch.bfloat16
+        assert w2.shape == (Q, self.d_h, self.d_e) and w2.dtype == torch.bfloat16
+        assert w13.is_cuda and w2.is_cuda and w13.is_contiguous() and w2.is_contiguous()
+        self.w13, self.w2 = w13, w2  # keep alive: the context stores raw pointers
+        st = lib.janus_moe_set_weights(self.ctx, self.instance, w13.data_ptr(), w2.data_ptr())
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+
+    def forward(self, x: torch.Tensor, experts: torch.Tensor, gate_w: torch.Tensor,
+                out: torch.Tensor | None = None, assign: dict | None = None) -> torch.Tensor:
+        """Device call on torch's current stream (asynchronous)."""
+        T = x.shape[0]
+        assert x.dtype == torch.bfloat16 and x.shape[1] == self.d_h and x.is_contiguous()
+        assert experts.dtype == torch.int32 and experts.numel() == T * self.k
+        assert gate_w.dtype == torch.float32 and gate_w.numel() == T * self.k
+        if out is None:
+            out = torch.empty_like(x)
+        a = None
+        if assign is not None:
+            a = JanusAssignment(**{k: (v.data_ptr() if v is not None else None)
+                                   for k, v in assign.items()})
+        st = lib.janus_moe_layer_async(self.ctx, x.data_ptr(), experts.data_ptr(),
+                                       gate_w.data_ptr(), T, out.data_ptr(),
+                                       C.byref(a) if a is not None else None,
+                                       _cur_stream(self.device))
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+        return out
+
+    def forward_host(self, x: torch.Tensor, experts: torch.Tensor, gate_w: torch.Tensor,
+                     out: torch.Tensor) -> torch.Tensor:
+        """End to end from (pinned) host tensors: H2D, layer, D2H, synchronise."""
+        T = x.shape[0]
+        st = lib.janus_moe_layer(self.ctx, x.data_ptr(), experts.data_ptr(), gate_w.data_ptr(), T,
+                                 out.data_ptr())
+        if st == EUNKNOWN_EXPERT:
+            raise ValidationError(self.sched.last_error())
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+        return out
+
+    def launches(self) -> int:
+        return self.sched.launches()
+
+
+def expert_weights(e: int, d_h: int, d_e: int, seed: int, device) -> tuple:
+    """Random-init SwiGLU expert e: N(0, 1/sqrt(fan_in)) bf16, seeded by
+    derive_seed(seed, "w", e).  Returns (wg [d_e,d_h], wu [d_e,d_h], wd [d_h,d_e])."""
+    g = torch.Generator(device=device)
+    g.manual_seed(derive_seed(seed, "w", e) & ((1 << 63) - 1))
+    wg = torch.randn(d_e, d_h, generator=g, device=device) * (d_h ** -0.5)
+    wu = torch.randn(d_e, d_h, generator=g, device=device) * (d_h ** -0.5)
+    wd = torch.randn(d_h, d_e, generator=g, device=device) * (d_e ** -0.5)
+    return wg.bfloat16(), wu.bfloat16(), wd.bfloat16()
+
+
+def build_weight_store(layer: MoELayer, seed: int) -> tuple:
+    """Weight store for ``layer`` from :func:`expert_weights` (replicas of one
+    expert share its weights)."""
+    experts = layer.local_experts()
+    Q = len(experts)
+    w13 = torch.empty(Q, 2 * layer.d_e, layer.d_h, dtype=torch.bfloat16, device=layer.device)
+    w2 = torch.empty(Q, layer.d_h, layer.d_e, dtype=torch.bfloat16, device=layer.device)
+    cache = {}
+    for q, e in enumerate(experts):
+        if e not in cache:
+            cache = {e: expert_weights(int(e), layer.d_h, layer.d_e, seed, layer.device)}
+        wg, wu, wd = cache[e]
+        w13[q, :layer.d_e] = wg
+        w13[q, layer.d_e:] = wu
+        w2[q] = wd
+    return w13, w2
+
+
+def make_inputs(T: int, k: int, d_h: int, seed: int, device) -> tuple:
+    """x ~ N(0,1) bf16 [T, d_h]; gate weights softmax of seeded N(0,1) logits over
+    the k slots, fp32 [T*k]."""
+    g = torch.Generator(device=device)
+    g.manual_seed(derive_seed(seed, "x", T) & ((1 << 63) - 1))
+    x = torch.randn(T, d_h, generator=g, device=device).bfloat16()
+    logits = torch.randn(T, k, generator=g, device=device)
+    gw = torch.softmax(logits, dim=1).reshape(-1).contiguous()
+    return x, gw

@@ -1,0 +1,134 @@
+"""CPU checks of the boundary: the C-ABI library loads and exports every symbol
+include/janus_b200.h declares; host-side functions of the product (synthetic
+routing, latency model, token sharding, text formats, validation) match the
+oracle / reference.  No compute kernels run here."""
+import ctypes as C
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(scope="module")
+def J():
+    import paper_2512_13525_b200 as J
+    return J
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "janus_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"\b(janus_[a-z_0-9]+)\s*\(", src))
+
+
+def test_library_exports_every_declared_symbol(J):
+    from paper_2512_13525_b200._lib import LIB_PATH, SYMBOLS
+    lib = C.CDLL(LIB_PATH)
+    declared = header_symbols()
+    assert declared == set(SYMBOLS)
+    for s in declared:
+        assert hasattr(lib, s), s
+
+
+def test_library_is_sm100a(J):
+    import subprocess
+    from paper_2512_13525_b200._lib import LIB_PATH
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+    sass = subprocess.run(["cuobjdump", "-sass", LIB_PATH], capture_output=True, text=True).stdout
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM", "MATCH.ANY"):
+        assert mnem in sass, mnem
+
+
+def test_gen_batch_matches_oracle(J, oracle):
+    for pat, cdf in ((J.RoutingPattern.gaussian(64, 0.15), oracle.pattern("gaussian", 64)[1]),
+                     (J.RoutingPattern.zipf(128, 1.0),
+                      oracle.pattern("pmf", 128, weights=[1 / (e + 1) for e in range(128)])[1]),
+                     (J.RoutingPattern.uniform(200), oracle.pattern("uniform", 200)[1])):
+        assert np.array_equal(pat.cdf, cdf)
+        for T in (0, 1, 255, 256, 4096):
+            b = J.gen_batch(pat, T, 8, 0x5EED, T)
+            assert np.array_equal(b.experts, oracle.gen_batch(cdf, T, 8, 0x5EED, T))
+
+
+def test_derive_seed(J, oracle):
+    for r, l, x in ((0, "a", 0), (42, "sched/random", 0), (7, "workload/step", 99)):
+        assert J.derive_seed(r, l, x) == oracle.derive_seed(r, l, x)
+
+
+def test_latency_model(J, oracle):
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        N = int(rng.integers(1, 9))
+        load = rng.integers(0, 30, N)
+        routed = rng.integers(0, 3000, N)
+        loads = [J.InstanceLoad(int(a), int(b)) for a, b in zip(load, routed)]
+        assert J.moe_layer_latency(loads, 2048, 768, 2, 1401.8e12, 6372.5e9, 5e-6) == \
+            oracle.moe_layer_latency(load, routed, 2048, 768)
+
+
+def test_shard_tokens():
+    import paper_2512_13525_b200 as J
+    # comm.cpp:76-81: even split, remainder to the lowest ids
+    for T, A in ((10, 3), (256, 2), (7, 8), (0, 4)):
+        cur = 0
+        for a in range(A):
+            first, count = J.shard_tokens(T, A, a)
+            assert first == cur and count == T // A + (a < T % A)
+            cur += count
+        assert cur == T
+
+
+def test_text_formats_round_trip(J, ref):
+    rcfg = "/root/reference/proj/configs"
+    if not os.path.isdir(rcfg):
+        pytest.skip("reference configs absent")
+    btxt = open(os.path.join(rcfg, "sample-batch.txt")).read()
+    mtxt = open(os.path.join(rcfg, "sample-replicas.txt")).read()
+    b = J.load_batch(btxt)
+    ex, T, k = ref.load_batch_text(btxt)
+    assert (b.num_tokens, b.top_k) == (T, k) and np.array_equal(b.experts, ex)
+    m = J.load_replica_map(mtxt)
+    rm = ref.load_replica_map_text(mtxt)
+    off, hosts, rid = m.csr()
+    assert np.array_equal(off, rm.off) and np.array_equal(hosts, rm.hosts)
+    assert np.array_equal(rid, rm.rid)
+
+
+def test_dump_assignment_format(J, ref):
+    g = json.load(open(os.path.join(GOLD, "sample_fixture.json")))
+    s = g["schedule"]
+    a = J.Assignment(*(np.array(s[f]) for f in ("instance", "replica", "expert_instance", "load",
+                                                "routed_tokens")))
+    b = J.ActivationBatch(g["T"], g["k"], g["experts"])
+    assert J.dump_assignment(a, b) == g["dump_assignment"]
+
+
+def test_validation_messages_match_reference(J, ref):
+    from oracle import CSRMap
+    cases = [
+        (2, 2, [[0], []]),
+        (2, 2, [[0], [3]]),
+        (2, 2, [[1, 0], [1]]),
+        (2, 1, [[0, 1], [0, 1]]),
+    ]
+    for N, C_, hosts in cases:
+        rids = [[0] * len(h) for h in hosts]
+        m = J.ReplicaMap(len(hosts), N, C_, hosts, rids)
+        with pytest.raises(J.ValidationError) as ei:
+            m.validate()
+        cm = CSRMap.from_lists(N, C_, hosts, rids)
+        assert ref.L.ref_map_validate(cm.E, cm.N, cm.C, cm.off, cm.hosts, cm.rid) == 1
+        assert str(ei.value) == ref.err()
+
+
+def test_config_maps_load(J):
+    for name in ("c1_uniform", "c1_gaussian", "c2", "c3", "c4_n2", "c4_n4", "c4_n8", "c5"):
+        m = J.config_map(name)
+        m.validate()
+        assert m.num_experts in (64, 128, 256)

@@ -1,0 +1,208 @@
+"""K3 permute + K4 grouped SwiGLU GEMMs + K5 combine on the GPU vs the fp32 CPU oracle.
+
+Tolerance: the device keeps h and y in bf16 between its
+kernels and rounds the output to bf16; the oracle computes in fp32 from the same
+bf16 inputs (h rounded to bf16 like the device).  Per element:
+    |out_dev - out_ref| <= RTOL * |out_ref| + ATOL * rms(out_ref)
+with RTOL = 2**-6 and ATOL = 2**-6.  Scheduling outputs inside the layer are
+checked bit-exact.
+"""
+import numpy as np
+import pytest
+
+from oracle import CSRMap, bf16_to_f32
+
+pytestmark = pytest.mark.gpu
+RTOL = 2.0 ** -6
+ATOL = 2.0 ** -6
+
+
+@pytest.fixture(scope="module")
+def J():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2512_13525_b200 as J
+    return J
+
+
+def u16(t):
+    import torch
+    return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def oracle_layer_out(oracle, layer, x, experts, gw, tokens=None):
+    """fp32 reference of out[t] for the given tokens (all by default).  For a
+    single-instance layer only the slots AEBS assigns to that instance count."""
+    T = x.shape[0]
+    k = layer.k
+    tokens = np.arange(T) if tokens is None else np.asarray(tokens)
+    xu = u16(x)
+    ex = experts.cpu().numpy().reshape(T, k)
+    if layer.instance >= 0:
+        off, hosts, rid = layer.sched._csr
+        m = CSRMap(layer.map.num_experts, layer.map.num_instances, layer.map.slots_per_instance,
+                   off, hosts, rid)
+        inst = oracle.schedule(ex.reshape(-1), T, k, m).instance.reshape(T, k)
+        ex = np.where(inst == layer.instance, ex, -1)
+    w = gw.cpu().numpy().reshape(T, k)
+    q_of = {}
+    for q, e in enumerate(layer.local_experts()):
+        q_of.setdefault(int(e), q)
+    d_e = layer.d_e
+    out = np.zeros((len(tokens), layer.d_h), np.float32)
+    by_e = {}
+    for i, t in enumerate(tokens):
+        for j in range(k):
+            by_e.setdefault(int(ex[t, j]), []).append((i, t, j))
+    for e, lst in by_e.items():
+        if e < 0 or e not in q_of:
+            continue  # routed to another instance (partial layer)
+        q = q_of[e]
+        w13 = u16(layer.w13[q])
+        wd = u16(layer.w2[q])
+        rows = np.stack([xu[t] for _, t, _ in lst])
+        y = oracle.expert_swiglu(rows, w13[:d_e], w13[d_e:], wd, round_h=True, nthreads=8)
+        for r, (i, t, j) in enumerate(lst):
+            out[i] += w[t, j] * y[r]
+    return out
+
+
+def check_close(dev, ref, what=""):
+    rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2))) or 1.0
+    err = np.abs(dev - ref)
+    bound = RTOL * np.abs(ref) + ATOL * rms
+    bad = err > bound
+    assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} outside tolerance; max err "
+                           f"{err.max():.4g}, rms(ref) {rms:.4g}")
+    return float(err.max() / rms)
+
+
+def make_layer(J, rmap, d_h, d_e, T_max, k, seed=1, instance=-1):
+    from paper_2512_13525_b200.moe import MoELayer, build_weight_store
+    layer = MoELayer(rmap, d_h, d_e, T_max, k, instance=instance)
+    w13, w2 = build_weight_store(layer, seed)
+    layer.set_weights(w13, w2)
+    return layer
+
+
+def run(J, layer, experts_np, T, seed=3):
+    import torch
+    from paper_2512_13525_b200.moe import make_inputs
+    x, gw = make_inputs(T, layer.k, layer.d_h, seed, "cuda")
+    ex = torch.from_numpy(np.ascontiguousarray(experts_np, np.int32)).cuda()
+    out = layer.forward(x, ex, gw)
+    torch.cuda.synchronize()
+    return x, ex, gw, out
+
+
+@pytest.mark.parametrize("T", [1, 5, 64, 300])
+def test_small_layer_all_tokens(J, oracle, T):
+    rm = J.ReplicaMap.from_hosts(1, 8, [[0]] * 8)
+    layer = make_layer(J, rm, 256, 128, 512, 2)
+    b = J.gen_batch(J.RoutingPattern.uniform(8), T, 2, 11, T)
+    x, ex, gw, out = run(J, layer, b.experts, T)
+    ref = oracle_layer_out(oracle, layer, x, ex, gw)
+    check_close(bf16_to_f32(u16(out)), ref, f"T={T}")
+
+
+def test_ragged_groups_multiple_n_tiles(J, oracle):
+    # 4 experts, 1000 tokens, k=2 -> groups of ~500 rows: 4+ n-tiles each, ragged tails
+    rm = J.ReplicaMap.from_hosts(1, 4, [[0]] * 4)
+    layer = make_layer(J, rm, 512, 256, 1000, 2)
+    b = J.gen_batch(J.RoutingPattern.zipf(4, 1.0), 1000, 2, 5, 0)
+    x, ex, gw, out = run(J, layer, b.experts, 1000)
+    ref = oracle_layer_out(oracle, layer, x, ex, gw)
+    check_close(bf16_to_f32(u16(out)), ref, "ragged")
+
+
+def test_replicated_map_all_instances_local(J, oracle):
+    # replicas of one expert share weights: the layer output must not depend on
+    # which replica AEBS picked
+    hosts = [[0, 1], [1, 2], [0, 2], [0], [1], [2], [0, 1, 2], [2]] * 2
+    rm = J.ReplicaMap.from_hosts(3, 12, hosts)
+    layer = make_layer(J, rm, 256, 128, 256, 4)
+    b = J.gen_batch(J.RoutingPattern.gaussian(16, 0.2), 200, 4, 9, 1)
+    x, ex, gw, out = run(J, layer, b.experts, 200)
+    ref = oracle_layer_out(oracle, layer, x, ex, gw)
+    check_close(bf16_to_f32(u16(out)), ref, "replicated")
+
+
+def test_per_instance_partials_sum_to_full(J, oracle):
+    import torch
+    hosts = [[0, 1], [1, 2], [0, 2], [0], [1], [2], [0, 1, 2], [2]] * 2
+    rm = J.ReplicaMap.from_hosts(3, 12, hosts)
+    b = J.gen_batch(J.RoutingPattern.gaussian(16, 0.2), 200, 4, 9, 1)
+    full = make_layer(J, rm, 256, 128, 256, 4)
+    x, ex, gw, out_full = run(J, full, b.experts, 200)
+    acc = torch.zeros(200, 256, dtype=torch.float32, device="cuda")
+    for g in range(3):
+        part = make_layer(J, rm, 256, 128, 256, 4, instance=g)
+        o = part.forward(x, ex, gw)
+        torch.cuda.synchronize()
+        ref_g = oracle_layer_out(oracle, part, x, ex, gw)
+        check_close(bf16_to_f32(u16(o)), ref_g, f"instance {g}")
+        acc += o.float()
+    check_close(acc.cpu().numpy(), bf16_to_f32(u16(out_full)), "sum of partials")
+
+
+def test_qwen3_30b_shape_sampled_tokens(J, oracle):
+    # c2: Qwen3-30B-A3B expert shape, the committed c2 map, Zipf-1.0 routing
+    rm = J.config_map("c2")
+    layer = make_layer(J, rm, 2048, 768, 256, 8)
+    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), 256, 8, 0x30, 256)
+    x, ex, gw, out = run(J, layer, b.experts, 256)
+    tokens = np.random.default_rng(0).choice(256, 48, replace=False)
+    ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens)
+    check_close(bf16_to_f32(u16(out))[tokens], ref, "c2 T=256")
+
+
+def test_layer_assignment_bit_exact_and_host_e2e(J, oracle):
+    import torch
+    from paper_maps import load_map_csr
+    m = load_map_csr("c3")
+    rm = J.config_map("c3")
+    layer = make_layer(J, rm, 256, 128, 512, 8)
+    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), 512, 8, 0x235, 512)
+    S, R = 512 * 8, int(m.off[-1])
+    d = lambda n, dt=torch.int32: torch.zeros(n, dtype=dt, device="cuda")
+    asg = dict(instance=d(S), replica=d(S), expert_instance=d(m.E), load=d(m.N),
+               routed_tokens=d(m.N, torch.int64), expert_tokens=None, slot_row=d(S),
+               row_slot=d(S), group_off=d(R + 1), status=d(2))
+    from paper_2512_13525_b200.moe import make_inputs
+    x, gw = make_inputs(512, 8, 256, 3, "cuda")
+    ex = torch.from_numpy(b.experts).cuda()
+    out = layer.forward(x, ex, gw, assign=asg)
+    torch.cuda.synchronize()
+    a = oracle.schedule(b.experts, 512, 8, m)
+    for f in ("instance", "replica", "expert_instance", "load", "routed_tokens"):
+        assert np.array_equal(asg[f].cpu().numpy(), getattr(a, f)), f
+    # host e2e path (pinned buffers) gives the identical bytes
+    xh = x.cpu().pin_memory()
+    eh = ex.cpu().pin_memory()
+    gh = gw.cpu().pin_memory()
+    oh = torch.empty(512, 256, dtype=torch.bfloat16).pin_memory()
+    layer.forward_host(xh, eh, gh, oh)
+    assert torch.equal(oh, out.cpu())
+
+
+def test_layer_rejects_unknown_expert(J):
+    import torch
+    rm = J.ReplicaMap.from_hosts(1, 4, [[0]] * 4)
+    layer = make_layer(J, rm, 256, 128, 16, 2)
+    x = torch.zeros(2, 256, dtype=torch.bfloat16).pin_memory()
+    ex = torch.tensor([0, 1, 2, 9], dtype=torch.int32).pin_memory()
+    gw = torch.ones(4, dtype=torch.float32).pin_memory()
+    out = torch.empty(2, 256, dtype=torch.bfloat16).pin_memory()
+    with pytest.raises(J.ValidationError, match="unknown-expert"):
+        layer.forward_host(x, ex, gw, out)
+
+
+def test_empty_step(J):
+    import torch
+    rm = J.ReplicaMap.from_hosts(1, 4, [[0]] * 4)
+    layer = make_layer(J, rm, 256, 128, 16, 2)
+    x = torch.zeros(0, 256, dtype=torch.bfloat16, device="cuda")
+    out = layer.forward(x, torch.zeros(0, dtype=torch.int32, device="cuda"),
+                        torch.zeros(0, dtype=torch.float32, device="cuda"))
+    torch.cuda.synchronize()
+    assert out.shape == (0, 256)
