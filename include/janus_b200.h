@@ -141,6 +141,11 @@ janus_status janus_moe_layer(janus_ctx *ctx, const void *x, const int32_t *exper
  * the number of layer calls recorded, and resets. */
 janus_status janus_profile(janus_ctx *ctx, int enable);
 janus_status janus_profile_read(janus_ctx *ctx, double *sched_ms, double *ffn_ms, int *calls);
+/* One scheduler pass over a device batch with in-kernel phase timestamps
+ * (%globaltimer, ns): ns[0..6] = start, loads issued + map staged, pass 1,
+ * scan + pins, sequential greedy, finish + scans, pass 2. */
+janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int num_tokens,
+                                  int top_k, int64_t *ns);
 
 /* ---- attention <-> MoE exchange (one NVLink box) ------------------------ */
 /* Token ownership on the attention side: even split, remainder to the lowest

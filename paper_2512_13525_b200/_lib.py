@@ -24,7 +24,7 @@ SYMBOLS = (
     "janus_time_schedule", "janus_moe_configure", "janus_moe_set_weights",
     "janus_moe_layer_async", "janus_moe_layer", "janus_shard_tokens",
     "janus_moe_layer_latency", "janus_gen_batch", "janus_derive_seed", "janus_profile",
-    "janus_profile_read",
+    "janus_profile_read", "janus_trace_schedule",
 )
 
 
@@ -66,6 +66,7 @@ def _load() -> C.CDLL:
     L.janus_derive_seed.restype = u64
     L.janus_profile.argtypes = [vp, i32]
     L.janus_profile_read.argtypes = [vp, P(dbl), P(dbl), P(i32)]
+    L.janus_trace_schedule.argtypes = [vp, vp, i32, i32, P(i64)]
     return L
 
 

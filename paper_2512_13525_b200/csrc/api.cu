@@ -258,6 +258,7 @@ static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T
   a.S = T * k;
   a.k = k;
   a.map = ctx->dmap;
+  a.id_bits = janus::id_bits_for(ctx->dmap.E);
   a.policy = policy;
   a.rng_state = janus_derive_seed(seed, "sched/random", 0);
   a.out = out;
@@ -426,7 +427,7 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
 janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *w13, const void *w2) {
   janus_status st = check_ready(ctx);
   if (st != JANUS_OK) return st;
-  if (!ctx->ffn.xp) return fail(ctx, JANUS_ESTATE, "moe: janus_moe_configure first");
+  if (!ctx->ffn.h) return fail(ctx, JANUS_ESTATE, "moe: janus_moe_configure first");
   if (!w13 || !w2 || instance >= ctx->dmap.N)
     return fail(ctx, JANUS_EINVAL, "moe: bad weight store");
   CK(cudaSetDevice(ctx->device));
@@ -451,6 +452,7 @@ janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int k = ctx->top_k;
   janus_assignment a = ctx->ws;
+  a.row_slot = nullptr;  // the inverse permutation is not needed by the layer
   if (assign) {  // caller wants the scheduling outputs: write into its buffers
     a.instance = assign->instance ? assign->instance : a.instance;
     a.replica = assign->replica ? assign->replica : a.replica;
@@ -459,7 +461,7 @@ janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_
     a.routed_tokens = assign->routed_tokens ? assign->routed_tokens : a.routed_tokens;
     a.expert_tokens = assign->expert_tokens ? assign->expert_tokens : a.expert_tokens;
     a.slot_row = assign->slot_row ? assign->slot_row : a.slot_row;
-    a.row_slot = assign->row_slot ? assign->row_slot : a.row_slot;
+    a.row_slot = assign->row_slot;  // opt-in: the layer permutes slot-major
     a.group_off = assign->group_off ? assign->group_off : a.group_off;
     a.status = assign->status ? assign->status : a.status;
   }
@@ -480,7 +482,7 @@ janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_
   if (ev) CK(cudaEventRecord(ev[1], s));
   janus::FfnPlan &p = ctx->ffn;
   cudaError_t e =
-      janus::launch_permute(d_x, a.row_slot, a.group_off, p.q_begin, p.q_end, k, p.d_h, p.xp, s);
+      janus::launch_permute(d_x, a.slot_row, a.instance, ctx->instance, T * k, k, p.d_h, p.xp, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "permute_kernel");
   int launches = 0;
   if (ev) CK(cudaEventRecord(ev[2], s));
@@ -490,7 +492,7 @@ janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_
   e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
                             d_out, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
-  ctx->launches += 2 + launches;
+  ctx->launches += 3 + launches;  // scheduler, permute, combine, GEMMs
   return JANUS_OK;
 }
 
@@ -518,6 +520,36 @@ janus_status janus_moe_layer(janus_ctx *ctx, const void *x, const int32_t *exper
     return fail(ctx, JANUS_EUNKNOWN_EXPERT,
                 "unknown-expert: batch references expert " + std::to_string(status[1]) +
                     " with no replica in the map");
+  return JANUS_OK;
+}
+
+janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int T, int k,
+                                  int64_t *ns) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  CK(cudaSetDevice(ctx->device));
+  st = grow_sched(ctx, T * k);
+  if (st != JANUS_OK) return st;
+  uint64_t *d_trace = nullptr;
+  CK(cudaMalloc(&d_trace, 8 * sizeof(uint64_t)));
+  CK(cudaMemset(d_trace, 0, 8 * sizeof(uint64_t)));
+  janus::SchedArgs a{};
+  a.experts = d_experts;
+  a.S = T * k;
+  a.k = k;
+  a.map = ctx->dmap;
+  a.id_bits = janus::id_bits_for(ctx->dmap.E);
+  a.policy = JANUS_POLICY_AEBS;
+  a.out = ctx->d_out;
+  a.trace = d_trace;
+  cudaError_t e = janus::launch_schedule(a, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  uint64_t h[8] = {0};
+  if (e == cudaSuccess) e = cudaMemcpy(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d_trace);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "janus_trace_schedule");
+  ctx->launches += 1;
+  for (int i = 0; i < 7; ++i) ns[i] = (int64_t)(h[i] - h[0]);
   return JANUS_OK;
 }
 

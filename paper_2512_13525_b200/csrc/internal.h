@@ -29,7 +29,15 @@ struct SchedArgs {
   uint64_t rng_state;  // derive_seed(seed, "sched/random")
   janus_assignment out;
   int32_t *tile_off;   // [R+1] n-tile prefix for the grouped GEMM (BN = kTileN), optional
+  uint64_t *trace;     // [7] phase timestamps (%globaltimer), optional
+  int id_bits;         // bits of the largest expert id (ballot-based peer matching)
 };
+
+inline int id_bits_for(int E) {
+  int b = 1;
+  while ((1 << b) < E) ++b;
+  return b;
+}
 
 // Launches the fused scheduler + layout kernel (aebs.cu).
 cudaError_t launch_schedule(const SchedArgs &a, cudaStream_t stream);
@@ -49,8 +57,9 @@ struct FfnPlan {
 };
 
 cudaError_t build_ffn_tensor_maps(FfnPlan &p);
-cudaError_t launch_permute(const void *x, const int32_t *row_slot, const int32_t *group_off,
-                           int q_begin, int q_end, int k, int d_h, void *xp, cudaStream_t s);
+cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
+                           int instance, int S, int k, int d_h, void *xp, cudaStream_t s);
+// gate/up GEMM with fused SwiGLU, then the down GEMM; 2 launches.
 cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
                        cudaStream_t s, int *launches);
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,

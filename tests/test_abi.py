@@ -41,7 +41,8 @@ def test_library_is_sm100a(J):
     out = subprocess.run(["cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
     sass = subprocess.run(["cuobjdump", "-sass", LIB_PATH], capture_output=True, text=True).stdout
-    for mnem in ("UTCHMMA", "UTMALDG", "LDTM", "MATCH.ANY"):
+    # tcgen05.mma / TMA / tcgen05.ld in the GEMMs; warp votes + REDUX in the scheduler
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM", "VOTE.ANY", "CREDUX"):
         assert mnem in sass, mnem
 
 
