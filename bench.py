@@ -354,6 +354,176 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_box(args):
+    """N > 1: one NVLink box split into A attention + M MoE GPUs
+    (BoxPlan.for_gpus: 1A+1E, 1A+3E, 2A+6E).  Same c2 expert shape as N=1; the
+    replica map is the reference placement for M instances (maps/c2_m{M}).
+    Weak scaling in the MoE sub-group: T = tokens x M per step, so every MoE GPU
+    sees ~T*k/M = tokens*k slots, as the single GPU does at N=1."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_13525_b200 as J
+    from paper_2512_13525_b200._lib import lib
+    from paper_2512_13525_b200.dist import BoxPlan, JanusBox
+    from paper_2512_13525_b200.moe import MoELayer, build_weight_store, make_inputs
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    plan = BoxPlan.for_gpus(ws)
+    A, M = plan.n_attn, plan.n_moe
+    T = args.tokens * M
+    role = plan.role(rank)
+    layer = None
+    if role == "moe":
+        rmap = J.config_map(MAP if M == 1 else f"{MAP}_m{M}")
+        layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=plan.instance(rank), device=local)
+        layer.set_weights(*build_weight_store(layer, seed=1))
+    box = JanusBox(plan, rank, T, D_H, K_TOP, layer=layer, device=local)
+    pat = J.RoutingPattern.zipf(E, 1.0)
+    batches = [torch.from_numpy(J.gen_batch(pat, T, K_TOP, SEED, T * 1000 + i).experts).to(dev)
+               for i in range(N_BATCHES)]
+    x, gw = make_inputs(T, K_TOP, D_H, 3, dev)
+    first, cnt = plan.shard(T, rank) if role == "attention" else (0, 0)
+    xs = x[first:first + cnt].contiguous()
+    gws = [gw[first * K_TOP:(first + cnt) * K_TOP].contiguous()] if role == "attention" else []
+    exs = [b[first * K_TOP:(first + cnt) * K_TOP].contiguous() for b in batches]
+    out = torch.empty(max(cnt, 1), D_H, dtype=torch.bfloat16, device=dev)
+    s = torch.cuda.current_stream(dev)
+    stream = s.cuda_stream
+    epoch = [0]
+
+    def step(i, xin=None, exin=None, gwin=None, o=None):
+        epoch[0] += 1
+        if role == "attention":
+            box.dispatch(xin if xin is not None else xs, exin if exin is not None else
+                         exs[i % N_BATCHES], gwin if gwin is not None else gws[0], T, epoch[0],
+                         stream)
+            box.combine(o if o is not None else out, T, epoch[0], stream)
+        else:
+            box.moe_step(T, epoch[0], stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    if layer is not None:
+        lib.janus_profile(layer.ctx, 1)
+    launches0 = box.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(s)
+        for i in range(args.steps):
+            step(i)
+        e1.record(s)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = box.launches() - launches0
+    ffn = [0.0, 0.0, 0.0]
+    if layer is not None:
+        a_, b_, c_ = C.c_double(), C.c_double(), C.c_int()
+        lib.janus_profile_read(layer.ctx, C.byref(a_), C.byref(b_), C.byref(c_))
+        lib.janus_profile(layer.ctx, 0)
+        ffn = [a_.value / max(c_.value, 1), b_.value / max(c_.value, 1), 1.0]
+    # dispatch kernel alone (attention ranks): events around the dispatch only,
+    # over extra steps after the timed region
+    disp_ms = 0.0
+    dist.barrier()
+    nd = 20
+    for i in range(nd):
+        epoch[0] += 1
+        if role == "attention":
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(s)
+            box.dispatch(xs, exs[i % N_BATCHES], gws[0], T, epoch[0], stream)
+            d1.record(s)
+            box.combine(out, T, epoch[0], stream)
+            torch.cuda.synchronize()
+            disp_ms += d0.elapsed_time(d1) / nd
+        else:
+            box.moe_step(T, epoch[0], stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    tvec = torch.tensor([ms, ffn[1], float(launches), disp_ms], device=dev)
+    allv = [torch.zeros_like(tvec) for _ in range(ws)]
+    dist.all_gather(allv, tvec)
+    ms_max = max(float(v[0]) for v in allv)
+    ffn_ms = max(float(v[1]) for v in allv)  # slowest MoE GPU's grouped GEMMs
+    launches_all = int(sum(float(v[2]) for v in allv))
+    disp_ms = max(float(v[3]) for v in allv)
+
+    # e2e through the host API: attention ranks copy their shard in from pinned
+    # host memory and their outputs back each step
+    if role == "attention":
+        xh = xs.cpu().pin_memory()
+        exh = [e.cpu().pin_memory() for e in exs]
+        gwh = gws[0].cpu().pin_memory()
+        oh = torch.empty(max(cnt, 1), D_H, dtype=torch.bfloat16).pin_memory()
+        xd, exd, gwd = torch.empty_like(xs), torch.empty_like(exs[0]), torch.empty_like(gws[0])
+    dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        if role == "attention":
+            xd.copy_(xh, non_blocking=True)
+            exd.copy_(exh[i % N_BATCHES], non_blocking=True)
+            gwd.copy_(gwh, non_blocking=True)
+            step(i, xd, exd, gwd, out)
+            oh.copy_(out, non_blocking=True)
+            torch.cuda.synchronize()
+        else:
+            step(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e2e_s = time.perf_counter() - t0
+    tt = torch.tensor([e2e_s], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_s = float(tt.item())
+    timed_out = box.timed_out()
+    if rank == 0:
+        value = T * args.steps / (ms_max / 1e3)
+        sends = plan.bytes_per_step(T, D_H, K_TOP)
+        send_bytes = sends[0][0]
+        hbm, tf_burst, tf_sus, src = peaks()
+        line = {
+            "metric": "moe_layer_tokens_per_s_per_gpu", "value": value, "unit": "tokens/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (gen_batch Zipf routing, random-init bf16 weights)",
+            "config": {"workload": f"c2 expert shape (Qwen3-30B-A3B: 128 experts, top-8, "
+                                   f"d_h 2048, d_e 768) on one NVLink box split {A} attention + "
+                                   f"{M} MoE GPUs; attention->MoE dispatch and MoE->attention "
+                                   f"combine by peer-memory kernels",
+                       "tokens_per_step": T, "tokens_per_moe_gpu": args.tokens,
+                       "replica_map": f"maps/{MAP if M == 1 else f'{MAP}_m{M}'}.map",
+                       "parallelism": f"{A}A+{M}E", "l2": "inputs > L2 (weights streamed)"},
+            "tokens_per_s_per_gpu": value / ws, "tokens_per_s_per_moe_gpu": value / M,
+            "roofline": {"bound": "hbm", "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
+                         "ffn_us_per_step": ffn_ms * 1e3, "achieved": None, "peak": hbm,
+                         "unit": "GB/s", "frac": None, "traffic": None,
+                         "peak_source": f"{src} (MEASURED_PEAKS.json)"},
+            "nvlink": {"dispatch_bytes_per_step_per_attention_gpu": send_bytes,
+                       "combine_bytes_per_step_per_attention_gpu": sends[0][1],
+                       "dispatch_us": disp_ms * 1e3,
+                       "dispatch_achieved_gbs": send_bytes / (disp_ms / 1e3) / 1e9
+                       if disp_ms > 0 else None,
+                       "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy "
+                                                         "per direction (fallback)"},
+            "e2e": {"value": T * args.steps / e2e_s, "unit": "tokens/s",
+                    "h2d_bytes_per_step": T * (D_H * 2 + K_TOP * 8),
+                    "d2h_bytes_per_step": T * D_H * 2},
+            "gpu_launches": launches_all, "timed_out": timed_out,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -367,6 +537,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
+    elif dist_env()[0] > 1:
+        run_box(args)
     else:
         run_ours(args)
 

@@ -152,6 +152,31 @@ janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int 
  * ids (comm.cpp:76-81).  Writes first token and count of shard a. */
 void janus_shard_tokens(int64_t num_tokens, int attn_instances, int a, int64_t *first,
                         int64_t *count);
+/* One process per GPU.  Ranks [0, n_attn) own token shards (attention side),
+ * ranks [n_attn, n_attn + n_moe) are MoE instances g = rank - n_attn (their
+ * context holds the replica map and instance g's weight store).  Every rank
+ * allocates one exchange region (identical layout) and exports it; each rank
+ * then maps all peers' regions (CUDA IPC over NVLink P2P). */
+janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int rank,
+                                  int max_tokens, int d_hidden, int top_k);
+janus_status janus_xfer_handle(const janus_ctx *ctx, uint8_t *handle /* 64 bytes */);
+janus_status janus_xfer_connect(janus_ctx *ctx, const uint8_t *handles /* world x 64, by rank */);
+/* device, attention rank a: push this rank's shard (janus_shard_tokens of the
+ * step's num_tokens) — rows x [T_a][d_h] bf16, experts / gate_w [T_a*k] — into
+ * every MoE rank, then publish `epoch` (> 0, increasing per step). */
+janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
+                                       const float *d_gate_w, int64_t num_tokens, uint64_t epoch,
+                                       void *stream);
+/* device, MoE rank: wait for every shard of `epoch`, run K1-K4 on the received
+ * step, and push this instance's per-token partial sums to their owners. */
+janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t num_tokens, uint64_t epoch,
+                                        void *stream);
+/* device, attention rank: wait for every MoE partial of `epoch` and reduce
+ * them (instance order, fp32) into out [T_a][d_h] bf16. */
+janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t num_tokens,
+                                      uint64_t epoch, void *stream);
+/* host: 1 if a wait exceeded its bound (a peer never published). */
+janus_status janus_xfer_status(janus_ctx *ctx, int *timed_out);
 
 /* ---- model / workload --------------------------------------------------- */
 /* The reference roofline prediction (latency.cpp:17-32), kept for comparison

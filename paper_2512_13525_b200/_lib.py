@@ -24,7 +24,9 @@ SYMBOLS = (
     "janus_time_schedule", "janus_moe_configure", "janus_moe_set_weights",
     "janus_moe_layer_async", "janus_moe_layer", "janus_shard_tokens",
     "janus_moe_layer_latency", "janus_gen_batch", "janus_derive_seed", "janus_profile",
-    "janus_profile_read", "janus_trace_schedule",
+    "janus_profile_read", "janus_trace_schedule", "janus_xfer_configure", "janus_xfer_handle",
+    "janus_xfer_connect", "janus_attn_dispatch_async", "janus_moe_layer_xfer_async",
+    "janus_attn_combine_async", "janus_xfer_status",
 )
 
 
@@ -67,6 +69,13 @@ def _load() -> C.CDLL:
     L.janus_profile.argtypes = [vp, i32]
     L.janus_profile_read.argtypes = [vp, P(dbl), P(dbl), P(i32)]
     L.janus_trace_schedule.argtypes = [vp, vp, i32, i32, P(i64)]
+    L.janus_xfer_configure.argtypes = [vp, i32, i32, i32, i32, i32, i32]
+    L.janus_xfer_handle.argtypes = [vp, C.c_char_p]
+    L.janus_xfer_connect.argtypes = [vp, C.c_char_p]
+    L.janus_attn_dispatch_async.argtypes = [vp, vp, vp, vp, i64, u64, vp]
+    L.janus_moe_layer_xfer_async.argtypes = [vp, i64, u64, vp]
+    L.janus_attn_combine_async.argtypes = [vp, vp, i64, u64, vp]
+    L.janus_xfer_status.argtypes = [vp, P(i32)]
     return L
 
 

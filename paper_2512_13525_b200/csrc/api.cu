@@ -142,6 +142,10 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->d_experts);
   dfree(ctx->d_gw);
   for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
+  for (void *p : ctx->xfer.opened) cudaIpcCloseMemHandle(p);
+  dfree(ctx->xfer.local);
+  dfree(ctx->xfer.counter);
+  dfree(ctx->xfer.err);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -441,15 +445,21 @@ janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *w13
   return JANUS_OK;
 }
 
-janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
-                                   const float *d_gate_w, int T, void *d_out,
-                                   const janus_assignment *assign, void *stream) {
+}  // extern "C"
+
+// The layer body shared by the single-GPU entry point and the MoE rank of the
+// box exchange: K1 schedule -> K3 permute -> K4 GEMMs -> K5 combine, where
+// the combine either writes `d_out` locally or (push_epoch != 0) pushes this
+// instance's partial sums into the owning attention ranks' memory.
+static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
+                              const float *d_gate_w, int T, void *d_out,
+                              const janus_assignment *assign, cudaStream_t s,
+                              unsigned long long push_epoch) {
   janus_status st = check_ready(ctx);
   if (st != JANUS_OK) return st;
   if (!ctx->moe_ready) return fail(ctx, JANUS_ESTATE, "moe: weights not set");
   if (T < 0 || T > ctx->max_tokens)
     return fail(ctx, JANUS_EINVAL, "moe: num_tokens outside [0, max_tokens]");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int k = ctx->top_k;
   janus_assignment a = ctx->ws;
   a.row_slot = nullptr;  // the inverse permutation is not needed by the layer
@@ -489,10 +499,139 @@ janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_
   e = janus::launch_ffn(p, a.group_off, ctx->ws_tile_off, s, &launches);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "grouped_gemm_kernel");
   if (ev) CK(cudaEventRecord(ev[3], s));
-  e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
-                            d_out, s);
+  if (push_epoch)
+    e = janus::launch_combine_push(ctx->xfer, p.y, a.slot_row, a.instance, d_gate_w, T,
+                                   push_epoch, s);
+  else
+    e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
+                              d_out, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
   ctx->launches += 3 + launches;  // scheduler, permute, combine, GEMMs
+  return JANUS_OK;
+}
+
+extern "C" {
+
+janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
+                                   const float *d_gate_w, int T, void *d_out,
+                                   const janus_assignment *assign, void *stream) {
+  return layer_run(ctx, d_x, d_experts, d_gate_w, T, d_out, assign,
+                   static_cast<cudaStream_t>(stream), 0);
+}
+
+// ------------------------------------------------ box exchange (K6) -----
+
+janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int rank, int max_tokens,
+                                  int d_h, int k) {
+  if (!ctx) return JANUS_EINVAL;
+  if (n_attn < 1 || n_moe < 1 || rank < 0 || rank >= n_attn + n_moe || max_tokens < 1 ||
+      d_h <= 0 || d_h % 8 || k < 1)
+    return fail(ctx, JANUS_EINVAL, "xfer: bad configuration");
+  if (n_attn + n_moe > 16 || n_moe > 32)
+    return fail(ctx, JANUS_EUNSUPPORTED, "xfer: at most 16 ranks in one box");
+  CK(cudaSetDevice(ctx->device));
+  janus::XferState &x = ctx->xfer;
+  if (x.local) cudaFree(x.local);
+  for (void *p : x.opened) cudaIpcCloseMemHandle(p);
+  dfree(x.counter);
+  dfree(x.err);
+  x = janus::XferState{};
+  x.rank = rank;
+  x.world = n_attn + n_moe;
+  x.A = n_attn;
+  x.M = n_moe;
+  x.d_h = d_h;
+  x.k = k;
+  x.T_max = max_tokens;
+  x.L = janus::xfer_layout(n_attn, n_moe, max_tokens, d_h, k);
+  CK(cudaMalloc(&x.local, x.L.bytes));
+  CK(cudaMemset(x.local, 0, x.L.bytes));
+  CK(dalloc(&x.counter, 1));
+  CK(dalloc(&x.err, 1));
+  CK(cudaMemset(x.counter, 0, sizeof(unsigned)));
+  CK(cudaMemset(x.err, 0, sizeof(int)));
+  x.peer_base.assign(x.world, nullptr);
+  x.peer_base[rank] = x.local;
+  ctx->xfer_ready = false;
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_handle(const janus_ctx *ctx, uint8_t *handle) {
+  if (!ctx || !ctx->xfer.local || !handle) return JANUS_ESTATE;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, ctx->xfer.local) != cudaSuccess) return JANUS_ECUDA;
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle, &h, 64);
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_connect(janus_ctx *ctx, const uint8_t *handles) {
+  if (!ctx || !ctx->xfer.local) return JANUS_ESTATE;
+  CK(cudaSetDevice(ctx->device));
+  janus::XferState &x = ctx->xfer;
+  for (int r = 0; r < x.world; ++r) {
+    if (r == x.rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + 64 * r, 64);
+    void *p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    x.peer_base[r] = p;
+    x.opened.push_back(p);
+  }
+  ctx->xfer_ready = true;
+  return JANUS_OK;
+}
+
+janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
+                                       const float *d_gate_w, int64_t T, uint64_t epoch,
+                                       void *stream) {
+  if (!ctx || !ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: not connected");
+  const janus::XferState &x = ctx->xfer;
+  if (x.rank >= x.A) return fail(ctx, JANUS_EINVAL, "xfer: dispatch from a non-attention rank");
+  if (T < 0 || T > x.T_max || epoch == 0)
+    return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens] or epoch 0");
+  cudaError_t e = janus::launch_dispatch(x, d_x, d_experts, d_gate_w, T, epoch,
+                                         static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "dispatch_kernel");
+  ctx->launches += 1;
+  return JANUS_OK;
+}
+
+janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoch, void *stream) {
+  if (!ctx || !ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: not connected");
+  const janus::XferState &x = ctx->xfer;
+  if (x.rank < x.A || ctx->instance != x.rank - x.A)
+    return fail(ctx, JANUS_EINVAL, "xfer: MoE rank must hold instance rank - n_attn");
+  if (T < 0 || T > x.T_max || epoch == 0)
+    return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens] or epoch 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = janus::launch_wait(x, true, epoch, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
+  ctx->launches += 1;
+  unsigned char *base = static_cast<unsigned char *>(x.local);
+  return layer_run(ctx, base + x.L.x_off, reinterpret_cast<const int32_t *>(base + x.L.ex_off),
+                   reinterpret_cast<const float *>(base + x.L.gw_off), (int)T, nullptr, nullptr, s,
+                   epoch);
+}
+
+janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, uint64_t epoch,
+                                      void *stream) {
+  if (!ctx || !ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: not connected");
+  const janus::XferState &x = ctx->xfer;
+  if (x.rank >= x.A) return fail(ctx, JANUS_EINVAL, "xfer: combine on a non-attention rank");
+  int64_t first = 0, Ta = 0;
+  janus_shard_tokens(T, x.A, x.rank, &first, &Ta);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = janus::launch_wait(x, false, epoch, s);
+  if (e == cudaSuccess) e = janus::launch_reduce_partials(x, d_out, Ta, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "reduce_partials_kernel");
+  ctx->launches += 2;
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_status(janus_ctx *ctx, int *timed_out) {
+  if (!ctx || !ctx->xfer.err) return JANUS_ESTATE;
+  CK(cudaMemcpy(timed_out, ctx->xfer.err, sizeof(int), cudaMemcpyDeviceToHost));
   return JANUS_OK;
 }
 

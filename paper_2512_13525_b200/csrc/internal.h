@@ -66,6 +66,36 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
                            cudaStream_t s);
 
+// Attention <-> MoE exchange (xfer.cu).  Ranks [0, A) own token shards,
+// ranks [A, A+M) are MoE instances g = rank - A.  One exchange region per
+// rank, identical layout everywhere.
+struct XferLayout {
+  size_t flag_dispatch_off, flag_combine_off, x_off, ex_off, gw_off, part_off, bytes;
+  long long ta_max;  // largest attention shard
+};
+XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k);
+
+struct XferState {
+  int rank = -1, world = 0, A = 0, M = 0, d_h = 0, k = 0;
+  long long T_max = 0;
+  XferLayout L{};
+  void *local = nullptr;              // this rank's exchange region
+  std::vector<void *> peer_base;      // every rank's region (mapped), by rank
+  std::vector<void *> opened;         // IPC mappings to close
+  unsigned *counter = nullptr;        // last-block counter (device)
+  int *err = nullptr;                 // wait timeout flag (device)
+};
+
+cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *d_ex,
+                            const float *d_gw, long long T, unsigned long long epoch,
+                            cudaStream_t s);
+cudaError_t launch_wait(const XferState &x, bool dispatch_flags, unsigned long long epoch,
+                        cudaStream_t s);
+cudaError_t launch_combine_push(const XferState &x, const void *y, const int32_t *slot_row,
+                                const int32_t *slot_inst, const float *gw, long long T,
+                                unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta, cudaStream_t s);
+
 }  // namespace janus
 
 struct janus_ctx {
@@ -95,6 +125,10 @@ struct janus_ctx {
   void *d_x = nullptr, *d_outbuf = nullptr;
   int32_t *d_experts = nullptr;
   float *d_gw = nullptr;
+
+  // attention <-> MoE exchange
+  bool xfer_ready = false;
+  janus::XferState xfer;
 
   // instrumentation (janus_profile)
   bool profiling = false;

@@ -1,0 +1,147 @@
+"""One NVLink box split into an attention sub-group and an MoE sub-group.
+
+Ranks ``[0, A)`` own token shards (the attention side: even split, remainder to
+the lowest ids, src/comm.cpp:76-81); ranks ``[A, A+M)`` are MoE instances
+``g = rank - A``, each holding the replicas AEBS may pick on instance g.  A
+decode step's MoE layer is
+
+  attention a:  janus_attn_dispatch_async  — push shard rows + routing + gate
+                weights into every MoE rank's memory (NVLink P2P stores), flag
+  MoE g:        janus_moe_layer_xfer_async — wait for all shards, K1 schedule
+                (replicated, identical on every MoE GPU: no count exchange),
+                K3/K4 on this instance's groups, K5 partial sums pushed straight
+                into the owners' memory, flag
+  attention a:  janus_attn_combine_async   — wait for the M partials, reduce
+                (fixed instance order) into the shard's output rows.
+
+torch.distributed is plumbing only: the one-time exchange of CUDA IPC handles.
+The data path is libjanus_b200.so's kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from ._lib import OK, lib
+from .moesim import JanusError, shard_tokens
+
+
+@dataclass(frozen=True)
+class BoxPlan:
+    """Roles and token ownership of an A-attention + M-MoE box (pure host logic)."""
+
+    n_attn: int
+    n_moe: int
+
+    @property
+    def world(self) -> int:
+        return self.n_attn + self.n_moe
+
+    def role(self, rank: int) -> str:
+        return "attention" if rank < self.n_attn else "moe"
+
+    def instance(self, rank: int) -> int:
+        return rank - self.n_attn if rank >= self.n_attn else -1
+
+    def shard(self, num_tokens: int, rank: int):
+        """(first, count) of attention rank's token shard (comm.cpp:76-81)."""
+        assert rank < self.n_attn
+        return shard_tokens(num_tokens, self.n_attn, rank)
+
+    def owner(self, num_tokens: int, t: int) -> int:
+        for a in range(self.n_attn):
+            first, count = self.shard(num_tokens, a)
+            if first <= t < first + count:
+                return a
+        raise ValueError(t)
+
+    def bytes_per_step(self, num_tokens: int, d_h: int, k: int):
+        """NVLink bytes each attention rank sends / receives per step."""
+        out = {}
+        for a in range(self.n_attn):
+            _, ta = self.shard(num_tokens, a)
+            send = self.n_moe * ta * (2 * d_h + 8 * k)
+            recv = self.n_moe * ta * 2 * d_h
+            out[a] = (send, recv)
+        return out
+
+    @staticmethod
+    def for_gpus(n: int) -> "BoxPlan":
+        """Default split used by the benches: 1 attention GPU per 4 (the paper's
+        example box is 2 attention + 6 MoE of 8)."""
+        a = max(1, n // 4)
+        return BoxPlan(a, n - a)
+
+
+class _Ctx:
+    """A bare device context (attention ranks hold no replica map)."""
+
+    def __init__(self, device: int):
+        self.ctx = C.c_void_p()
+        st = lib.janus_create(C.byref(self.ctx), device)
+        if st != OK:
+            raise JanusError(st, f"janus_create(device={device})")
+
+    def last_error(self) -> str:
+        return lib.janus_last_error(self.ctx).decode()
+
+
+class JanusBox:
+    """This rank's endpoint of the box exchange.
+
+    For an MoE rank pass ``layer`` (a :class:`paper_2512_13525_b200.moe.MoELayer`
+    built with ``instance = rank - n_attn`` and its weight store set)."""
+
+    def __init__(self, plan: BoxPlan, rank: int, max_tokens: int, d_hidden: int, top_k: int,
+                 layer=None, device: int = 0, group=None):
+        import torch.distributed as dist
+        self.plan, self.rank = plan, rank
+        self.max_tokens, self.d_h, self.k = max_tokens, d_hidden, top_k
+        if plan.role(rank) == "moe":
+            if layer is None or layer.instance != plan.instance(rank):
+                raise ValueError("an MoE rank needs its MoELayer with instance = rank - n_attn")
+            self.layer = layer
+            self._ctx = layer.ctx
+            self._err = layer.sched.last_error
+        else:
+            self.layer = None
+            self._c = _Ctx(device)
+            self._ctx = self._c.ctx
+            self._err = self._c.last_error
+        self._check(lib.janus_xfer_configure(self._ctx, plan.n_attn, plan.n_moe, rank, max_tokens,
+                                             d_hidden, top_k))
+        h = C.create_string_buffer(64)
+        self._check(lib.janus_xfer_handle(self._ctx, h))
+        handles = [None] * plan.world
+        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        self._check(lib.janus_xfer_connect(self._ctx, b"".join(handles)))
+        dist.barrier(group=group)
+
+    def _check(self, st):
+        if st != OK:
+            raise JanusError(st, self._err())
+
+    # --- attention rank ------------------------------------------------------
+    def dispatch(self, x_shard, experts_shard, gate_w_shard, num_tokens: int, epoch: int,
+                 stream: int) -> None:
+        self._check(lib.janus_attn_dispatch_async(self._ctx, x_shard.data_ptr(),
+                                                  experts_shard.data_ptr(),
+                                                  gate_w_shard.data_ptr(), num_tokens, epoch,
+                                                  stream))
+
+    def combine(self, out_shard, num_tokens: int, epoch: int, stream: int) -> None:
+        self._check(lib.janus_attn_combine_async(self._ctx, out_shard.data_ptr(), num_tokens,
+                                                 epoch, stream))
+
+    # --- MoE rank ---------------------------------------------------------------
+    def moe_step(self, num_tokens: int, epoch: int, stream: int) -> None:
+        self._check(lib.janus_moe_layer_xfer_async(self._ctx, num_tokens, epoch, stream))
+
+    def timed_out(self) -> bool:
+        v = C.c_int()
+        self._check(lib.janus_xfer_status(self._ctx, C.byref(v)))
+        return bool(v.value)
+
+    def launches(self) -> int:
+        return int(lib.janus_launch_count(self._ctx))
+

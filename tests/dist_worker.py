@@ -1,0 +1,89 @@
+"""Multi-GPU worker for tests/test_gpu_dist.py (launched with torchrun, one rank
+per GPU).  Runs several decode steps of an A-attention + M-MoE box through the
+C-ABI exchange and checks every attention shard's output against the same
+layer computed on one GPU (instance -1, all replicas local).
+
+  torchrun --nproc-per-node A+M tests/dist_worker.py --attn A --moe M --out DIR
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2512_13525_b200 as J  # noqa: E402
+from paper_2512_13525_b200.dist import BoxPlan, JanusBox  # noqa: E402
+from paper_2512_13525_b200.moe import MoELayer, build_weight_store, make_inputs  # noqa: E402
+
+RTOL = ATOL = 2.0 ** -6
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--attn", type=int, default=1)
+    ap.add_argument("--moe", type=int, default=1)
+    ap.add_argument("--tokens", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--out", default="gpurun_out")
+    args = ap.parse_args()
+    rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    plan = BoxPlan(args.attn, args.moe)
+    assert dist.get_world_size() == plan.world
+    E, k, d_h, d_e, T = 16, 4, 256, 128, args.tokens
+    M = plan.n_moe
+    hosts = [sorted({e % M, (e + 1) % M}) for e in range(E)]
+    rmap = J.ReplicaMap.from_hosts(M, E, hosts)
+    dev = torch.device("cuda", local)
+
+    layer = None
+    if plan.role(rank) == "moe":
+        layer = MoELayer(rmap, d_h, d_e, T, k, instance=plan.instance(rank), device=local)
+        layer.set_weights(*build_weight_store(layer, seed=1))
+    box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local)
+    full = None
+    if plan.role(rank) == "attention":
+        full = MoELayer(rmap, d_h, d_e, T, k, instance=-1, device=local)
+        full.set_weights(*build_weight_store(full, seed=1))
+
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    result = {"rank": rank, "role": plan.role(rank), "steps": []}
+    for step in range(1, args.steps + 1):
+        Ts = T - 37 * (step % 3)  # vary the step size: ragged shards
+        b = J.gen_batch(J.RoutingPattern.gaussian(E, 0.2), Ts, k, 7, step)
+        x, gw = make_inputs(Ts, k, d_h, step, dev)
+        ex = torch.from_numpy(b.experts).to(dev)
+        if plan.role(rank) == "attention":
+            first, cnt = plan.shard(Ts, rank)
+            out = torch.empty(cnt, d_h, dtype=torch.bfloat16, device=dev)
+            box.dispatch(x[first:first + cnt].contiguous(), ex[first * k:(first + cnt) * k],
+                         gw[first * k:(first + cnt) * k], Ts, step, stream)
+            box.combine(out, Ts, step, stream)
+            ref = full.forward(x, ex, gw)[first:first + cnt]
+            torch.cuda.synchronize()
+            o, r = out.float().cpu().numpy(), ref.float().cpu().numpy()
+            rms = float(np.sqrt(np.mean(r.astype(np.float64) ** 2))) or 1.0
+            bad = int((np.abs(o - r) > RTOL * np.abs(r) + ATOL * rms).sum())
+            result["steps"].append({"T": Ts, "shard": [first, cnt], "bad": bad,
+                                    "max_err_over_rms": float(np.abs(o - r).max() / rms)})
+        else:
+            box.moe_step(Ts, step, stream)
+            torch.cuda.synchronize()
+            result["steps"].append({"T": Ts})
+    result["timed_out"] = box.timed_out()
+    os.makedirs(args.out, exist_ok=True)
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_rank{rank}.json"), "w") as f:
+        json.dump(result, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
