@@ -93,11 +93,24 @@ __global__ void dispatch_kernel(PeerPtrs peers, int M, int A, int a, const uint4
                                 unsigned long long epoch, unsigned *counter) {
   const long long nx = Ta * vec, ns = Ta * k;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nx; i += stride) {
-    const uint4 v = __ldg(x + i);
+  // 4 independent 16-B chunks per thread per round: 4 loads in flight, then
+  // 4*M posted peer stores.
+  constexpr int U = 4;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < nx;
+       i0 += stride * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < nx) v[u] = __ldg(x + i);
+    }
     for (int g = 0; g < M; ++g) {
       uint4 *dst = reinterpret_cast<uint4 *>(peers.base[A + g] + L.x_off) + first * vec;
-      dst[i] = v;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long i = i0 + u * stride;
+        if (i < nx) dst[i] = v[u];
+      }
     }
   }
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ns; i += stride) {
