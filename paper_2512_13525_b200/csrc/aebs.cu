@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
       const int q = s_qidx[p];
       qof[e] = q;
       qcnt[q] = tot[e];
-      tcnt[q] = (tot[e] + kTileN - 1) / kTileN;
+      tcnt[q] = (tot[e] + a.tile_n - 1) / a.tile_n;
       atomicAdd(&routed[g], (unsigned)tot[e]);
     }
     if (leader) {

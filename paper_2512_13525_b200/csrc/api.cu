@@ -3,6 +3,7 @@
 // live in aebs.cu / ffn.cu.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -90,6 +91,13 @@ uint64_t hash_label(const char *label) {
   return h;
 }
 
+// Captured layer graphs bake in buffers and tensor maps: drop them whenever
+// the map, the workspace or the weight store changes.
+void clear_graphs(janus_ctx *ctx) {
+  for (auto &g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+}
+
 janus_status check_ready(janus_ctx *ctx) {
   if (!ctx) return JANUS_EINVAL;
   if (!ctx->have_map) return fail(ctx, JANUS_ESTATE, "janus: no replica map set");
@@ -115,6 +123,8 @@ janus_status janus_create(janus_ctx **out, int device) {
   *out = nullptr;
   janus_ctx *ctx = new janus_ctx();
   ctx->device = device;
+  const char *g = std::getenv("JANUS_GRAPH");
+  ctx->use_graph = !(g && g[0] == '0');
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
@@ -142,6 +152,8 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->d_experts);
   dfree(ctx->d_gw);
   for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
+  for (auto &g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (void *p : ctx->xfer.opened) cudaIpcCloseMemHandle(p);
   dfree(ctx->xfer.local);
   dfree(ctx->xfer.counter);
@@ -234,6 +246,7 @@ janus_status janus_set_replica_map(janus_ctx *ctx, int E, int N, int C, const in
   m.C = C;
   m.R = R;
   ctx->have_map = true;
+  clear_graphs(ctx);
   // a new map invalidates the layer's weight store
   ctx->moe_ready = false;
   ctx->ffn.w13 = ctx->ffn.w2 = nullptr;
@@ -267,6 +280,7 @@ static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T
   a.rng_state = janus_derive_seed(seed, "sched/random", 0);
   a.out = out;
   a.tile_off = tile_off;
+  a.tile_n = ctx->ffn.tile_n > 0 ? ctx->ffn.tile_n : janus::kTileN;
   cudaError_t e = janus::launch_schedule(a, stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aebs_schedule_kernel");
   ctx->launches += 1;
@@ -425,6 +439,7 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   ctx->ffn.d_e = d_e;
   ctx->ffn.S_alloc = S_alloc;
   ctx->moe_ready = false;
+  clear_graphs(ctx);
   return JANUS_OK;
 }
 
@@ -442,6 +457,7 @@ janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *w13
   ctx->ffn.w2 = w2;
   CK(janus::build_ffn_tensor_maps(ctx->ffn));
   ctx->moe_ready = true;
+  clear_graphs(ctx);
   return JANUS_OK;
 }
 
@@ -475,6 +491,9 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     a.group_off = assign->group_off ? assign->group_off : a.group_off;
     a.status = assign->status ? assign->status : a.status;
   }
+  // GEMM n-tile: decode steps (few rows per replica group) use 64-row tiles
+  // and the deep 9-stage weight ring; larger steps 256-row tiles
+  ctx->ffn.tile_n = (int64_t)T * k <= 48LL * ctx->dmap.E ? 64 : janus::kTileN;
   cudaEvent_t *ev = nullptr;
   if (ctx->profiling) {
     const size_t need = 4 * (size_t)(ctx->prof_calls + 1);
@@ -506,17 +525,60 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
                               d_out, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
-  ctx->launches += 3 + launches;  // scheduler, permute, combine, GEMMs
+  ctx->launches += 2 + launches;  // permute, combine, GEMMs (launch_sched counts itself)
   return JANUS_OK;
 }
 
 extern "C" {
 
+// The layer's kernel sequence is captured once per (buffers, T) into a CUDA
+// graph and replayed: one launch per step instead of five, no host work per
+// kernel.  Disabled while profiling (events), when the caller asks for the
+// scheduling outputs, or with JANUS_GRAPH=0.
 janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                                    const float *d_gate_w, int T, void *d_out,
                                    const janus_assignment *assign, void *stream) {
-  return layer_run(ctx, d_x, d_experts, d_gate_w, T, d_out, assign,
-                   static_cast<cudaStream_t>(stream), 0);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!ctx || !ctx->use_graph || ctx->profiling || assign)
+    return layer_run(ctx, d_x, d_experts, d_gate_w, T, d_out, assign, s, 0);
+  const janus_ctx::GraphKey key{d_x, d_experts, d_gate_w, d_out, T};
+  janus_ctx::GraphEntry *hit = nullptr;
+  for (auto &g : ctx->graphs)
+    if (g.key == key) hit = &g;
+  if (!hit) {
+    constexpr size_t kMaxGraphs = 16;
+    if (ctx->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+      auto lru = std::min_element(ctx->graphs.begin(), ctx->graphs.end(),
+                                  [](const auto &a, const auto &b) {
+                                    return a.last_use < b.last_use;
+                                  });
+      cudaGraphExecDestroy(lru->exec);
+      ctx->graphs.erase(lru);
+    }
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    const uint64_t before = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    janus_status st = layer_run(ctx, d_x, d_experts, d_gate_w, T, d_out, nullptr,
+                                ctx->cap_stream, 0);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
+    if (st != JANUS_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+    ctx->graphs.push_back({key, exec, ctx->launches - before, 0});
+    ctx->launches = before;
+    hit = &ctx->graphs.back();
+  }
+  hit->last_use = ++ctx->graph_clock;
+  CK(cudaGraphLaunch(hit->exec, s));
+  ctx->launches += hit->kernels;
+  return JANUS_OK;
 }
 
 // ------------------------------------------------ box exchange (K6) -----
@@ -681,6 +743,7 @@ janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int 
   a.policy = JANUS_POLICY_AEBS;
   a.out = ctx->d_out;
   a.trace = d_trace;
+  a.tile_n = janus::kTileN;
   cudaError_t e = janus::launch_schedule(a, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   uint64_t h[8] = {0};

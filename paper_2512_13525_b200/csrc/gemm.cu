@@ -1,0 +1,545 @@
+// gemm.cu — K4: the grouped SwiGLU expert GEMMs on tcgen05 CTA pairs, TMA and
+// TMEM.  sm_100a only.
+//
+// The expert FFN has no reference implementation: the reference models it as
+// t_launch + max(A*W_e/beta, 2*b*d_h*d_e/pi) (src/latency.cpp:17-24).  Here it
+// is computed for real:
+//   h = silu(x Wg^T) * (x Wu^T)          (kernel mode SWIGLU, h kept in bf16)
+//   y = h Wd^T                           (kernel mode PLAIN)
+//
+// Grouped GEMM, swap-AB, on CTA pairs.  The weight rows are the UMMA M side,
+// the ragged token rows of one replica group the N side, K the reduction dim.
+// A tile is one replica group q x 256 weight rows x <=256 token rows, computed
+// by a cluster of 2 CTAs with tcgen05.mma.cta_group::2 (M=256): CTA r holds
+// 128 weight rows of A and half of the token rows of B in its own smem, the
+// pair's tensor cores share both halves, and CTA r's TMEM accumulates its 128
+// rows x N columns.  Per SM and k-block that is 32 KB written by TMA and 32 KB
+// read by the MMAs — half the smem traffic of two independent M=128 tiles,
+// which capped the single-CTA version at ~58% of the tensor pipe (profiles/).
+//   SWIGLU  CTA r's 128 rows = 64 gate rows + the 64 up rows of the same
+//           features (two TMA boxes), so the epilogue pairs lanes l and l+64
+//           through a small smem exchange and writes h for 64 features.
+//   PLAIN   CTA r's 128 rows = 128 consecutive rows of the down projection.
+// Per CTA: warp 0 TMA producer, warp 1 TMEM owner (+ the MMA issuer in the
+// leader CTA), warps 2-5 epilogue (tcgen05.ld -> math -> bf16 -> smem ->
+// coalesced 16-B stores).  6-stage smem ring, 2 TMEM accumulators of 256
+// columns.  Persistent: 74 pairs walk the tile list that the scheduler kernel
+// wrote to device memory (group_off, tile_off) — no host sync.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace janus {
+namespace {
+
+constexpr int kBK = 64;                        // K elements per stage (128-B rows, SW128)
+constexpr int kATileBytes = 128 * kBK * 2;     // 16 KB: this CTA's 128 weight rows
+constexpr int kEpiCols = 32;                   // token columns per epilogue chunk
+constexpr int kStagingBytes = kEpiCols * 128 * 2;     // 32 rows x 128 bf16
+constexpr int kXchgBytes = 128 * (kEpiCols + 1) * 4;  // SwiGLU exchange, padded rows
+constexpr int kGemmThreads = 192;
+constexpr int kTmemCols = 512;                 // 2 accumulators x 256 columns
+
+// Two shapes of the smem ring, chosen per launch from the expected rows per
+// replica group (api.cu): BH = token rows per CTA per tile (pair N = 2*BH).
+//   BH=128  6 stages x (16 KB A + 16 KB B): the tensor-bound regime (N=256)
+//   BH=32   9 stages x (16 KB A +  4 KB B): decode, 144 KB of weights in flight
+template <int BH>
+struct Ring {
+  static constexpr int kBTileBytes = BH * kBK * 2;
+  static constexpr int kStageBytes = kATileBytes + kBTileBytes;
+  static constexpr int kStages = BH == 128 ? 6 : 9;
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kStagingBytes + kXchgBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+enum Mode { kSwiglu = 0, kPlain = 1 };
+
+struct GemmParams {
+  CUtensorMap tm_a;     // weights [Q*M_per_q][K]; box 64 rows (SWIGLU) / 128 rows (PLAIN)
+  CUtensorMap tm_b[5];  // activations [S_alloc][K], box rows 8/16/32/64/128 (= N/2)
+  const int32_t *group_off;
+  const int32_t *tile_off;  // n-tiles of tile_n rows per group (prefix)
+  int tile_n;     // token rows per tile (= 2*BH)
+  int q_begin, q_end;
+  int K;          // reduction length
+  int m_tiles;    // weight blocks per group (SWIGLU: 128 features, PLAIN: 256)
+  int m_per_q;    // weight rows per replica
+  int up_off;     // SWIGLU: row offset of the up projection (d_e)
+  __nv_bfloat16 *out;
+  int out_ld;     // elements per output row
+};
+
+// ---------------------------------------------------------------- PTX -----
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// Cluster-window address of the same smem variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// Arrive on an mbarrier in another CTA of the cluster (cluster-window address).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// TMA 2-D tile load by either CTA of the pair; completion bytes are counted on
+// the leader CTA's mbarrier (cluster-window address).
+__device__ __forceinline__ void tma_load_pair(void *dst, const CUtensorMap *tm, uint32_t bar_leader,
+                                              int x, int y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar_leader), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// SW128 K-major smem matrix descriptor (cute::UMMA::SmemDescriptor layout):
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4
+// [32,46) = 1024 B between 8-row groups, version 1 [46,48), layout 2 = 128B
+// swizzle [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=256 (pair).
+__device__ __forceinline__ uint32_t idesc_bf16_m256(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((256u >> 4) << 24);
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// Arrive (once) on the mbarrier at this smem offset in both CTAs of the pair
+// when every previously issued MMA of this thread has completed.
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct TileCoord {
+  int q, m, r0, rows, half;  // half = N/2 token rows loaded by each CTA
+};
+
+// Tile t (relative to the first tile of q_begin) -> (group, m-block, rows).
+// The list is walked zig-zag (t even: from the front, odd: from the back) so
+// that the pairs running at the same moment mix the hot groups' tensor-bound
+// tiles with the cold groups' weight-streaming tiles: replica order follows
+// placement order, which is by descending load (experts.cpp place_replicas).
+__device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in, int total) {
+  const int t = (t_in & 1) ? total - 1 - (t_in >> 1) : (t_in >> 1);
+  const int base = p.tile_off[p.q_begin];
+  int lo = p.q_begin, hi = p.q_end;  // find q: (tile_off[q]-base)*m <= t < (tile_off[q+1]-base)*m
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if ((p.tile_off[mid] - base) * p.m_tiles <= t) lo = mid;
+    else hi = mid;
+  }
+  const int q = lo;
+  const int nt = p.tile_off[q + 1] - p.tile_off[q];
+  const int local = t - (p.tile_off[q] - base) * p.m_tiles;
+  TileCoord c;
+  c.q = q;
+  c.m = local / nt;
+  const int n = local % nt;
+  c.r0 = p.group_off[q] + n * p.tile_n;
+  c.rows = min(p.tile_n, p.group_off[q + 1] - c.r0);
+  const int need = (c.rows + 1) / 2;  // rows per CTA
+  c.half = need <= 8 ? 8 : need <= 16 ? 16 : need <= 32 ? 32 : need <= 64 ? 64 : 128;
+  return c;
+}
+
+__device__ __forceinline__ int box_index(int half) {
+  return half == 8 ? 0 : half == 16 ? 1 : half == 32 ? 2 : half == 64 ? 3 : 4;
+}
+
+template <int MODE, int BH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
+  constexpr int kStages = Ring<BH>::kStages;
+  constexpr int kStageBytes = Ring<BH>::kStageBytes;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char *stage_base = smem;
+  __nv_bfloat16 *staging = reinterpret_cast<__nv_bfloat16 *>(smem + kStages * kStageBytes);
+  float *xchg = reinterpret_cast<float *>(smem + kStages * kStageBytes + kStagingBytes);
+  uint64_t *bars =
+      reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes + kStagingBytes + kXchgBytes);
+  uint64_t *full = bars;                      // [kStages] leader: TMA bytes of both CTAs
+  uint64_t *empty = bars + kStages;           // [kStages] both: MMA done with the stage
+  uint64_t *tfull = bars + 2 * kStages;       // [2]       both: accumulator ready
+  uint64_t *tempty = bars + 2 * kStages + 2;  // [2]       leader: both epilogues drained it
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * kStages + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int total = (p.tile_off[p.q_end] - p.tile_off[p.q_begin]) * p.m_tiles;
+  const int kblocks = p.K / kBK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tm_a);
+    for (int i = 0; i < 5; ++i) prefetch_tmap(&p.tm_b[i]);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+      const uint64_t pol_x = policy_evict_last();   // token rows: reused by every m-block
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total; t += npairs) {
+        const TileCoord c = tile_coord(p, t, total);
+        const int bi = box_index(c.half);
+        const uint32_t bytes_pair = 2u * (kATileBytes + (uint32_t)c.half * kBK * 2);
+        const int rowq = (c.q - p.q_begin) * p.m_per_q;
+        const int brow = c.r0 + (int)crank * c.half;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char *sa = stage_base + stage * kStageBytes;
+          const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
+          if (leader) mbar_expect_tx(&full[stage], bytes_pair);
+          if (MODE == kSwiglu) {
+            const int f0 = c.m * 128 + (int)crank * 64;  // this CTA's 64 features
+            tma_load_pair(sa, &p.tm_a, bar, kb * kBK, rowq + f0, pol_w);
+            tma_load_pair(sa + kATileBytes / 2, &p.tm_a, bar, kb * kBK, rowq + p.up_off + f0,
+                          pol_w);
+          } else {
+            tma_load_pair(sa, &p.tm_a, bar, kb * kBK, rowq + c.m * 256 + (int)crank * 128, pol_w);
+          }
+          tma_load_pair(sa + kATileBytes, &p.tm_b[bi], bar, kb * kBK, brow, pol_x);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < total; t += npairs) {
+        const TileCoord c = tile_coord(p, t, total);
+        const uint32_t idesc = idesc_bf16_m256(2 * c.half);
+        const uint32_t d = tmem_base + acc * 256;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(stage_base + stage * kStageBytes);
+          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kATileBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5, both CTAs) =====================
+    const int quad = warp & 3;        // TMEM lanes quad*32 .. +31
+    const int et = threadIdx.x - 64;  // 0..127
+    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa(smem_u32(&tempty[1]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < total; t += npairs) {
+      const TileCoord c = tile_coord(p, t, total);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t d = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
+      // accumulator column j <-> token row r0 + j (CTA 0 loaded rows [0, half),
+      // CTA 1 rows [half, 2*half) of the tile)
+      for (int c0 = 0; c0 < c.rows; c0 += kEpiCols) {
+        const int rows = min(kEpiCols, c.rows - c0);
+        float v[32];
+        if (MODE == kSwiglu) {
+          // lanes 0..63 hold the gate projection, lanes 64..127 the up
+          // projection of the same 64 features: every warp parks its rows in
+          // smem, then all 128 threads each finish 16 (feature, column) pairs.
+          tmem_ld32(d + c0, v);
+          {
+            float *xr = xchg + (quad * 32 + lane) * (kEpiCols + 1);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xr[j] = v[j];
+          }
+          named_bar(1, 128);
+          {
+            const int f = et & 63, j0 = (et >> 6) * 16;
+            const float *gr = xchg + f * (kEpiCols + 1);
+            const float *ur = xchg + (64 + f) * (kEpiCols + 1);
+#pragma unroll
+            for (int j = j0; j < j0 + 16; ++j) {
+              const float g = gr[j];
+              staging[j * 64 + f] = __float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * ur[j]);
+            }
+          }
+          named_bar(1, 128);
+          __nv_bfloat16 *obase =
+              p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 128 + (int)crank * 64;
+          for (int i = et; i < rows * 8; i += 128) {  // 64 features = 8 x 16 B per row
+            const int r = i >> 3, ch = i & 7;
+            *reinterpret_cast<uint4 *>(obase + (size_t)r * p.out_ld + ch * 8) =
+                *reinterpret_cast<const uint4 *>(staging + r * 64 + ch * 8);
+          }
+          named_bar(1, 128);
+        } else {
+          tmem_ld32(d + c0, v);
+          const int f = quad * 32 + lane;  // 0..127
+#pragma unroll
+          for (int j = 0; j < 32; ++j) staging[j * 128 + f] = __float2bfloat16_rn(v[j]);
+          named_bar(1, 128);
+          __nv_bfloat16 *obase =
+              p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 256 + (int)crank * 128;
+          for (int i = et; i < rows * 16; i += 128) {  // 128 features = 16 x 16 B per row
+            const int r = i >> 4, ch = i & 15;
+            *reinterpret_cast<uint4 *>(obase + (size_t)r * p.out_ld + ch * 8) =
+                *reinterpret_cast<const uint4 *>(staging + r * 128 + ch * 8);
+          }
+          named_bar(1, 128);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                              const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                              const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows][cols] tensor map, box {64, box_rows}, 128B swizzle.
+bool make_map(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t build_ffn_tensor_maps(FfnPlan &p) {
+  const int Q = p.q_end - p.q_begin;
+  bool ok = make_map(&p.tm_w13, p.w13, (uint64_t)Q * 2 * p.d_e, p.d_h, 64) &&
+            make_map(&p.tm_w2, p.w2, (uint64_t)Q * p.d_h, p.d_e, 128);
+  for (int i = 0; i < 5 && ok; ++i) {
+    ok = make_map(&p.tm_xp[i], p.xp, p.S_alloc, p.d_h, 8u << i) &&
+         make_map(&p.tm_h[i], p.h, p.S_alloc, p.d_e, 8u << i);
+  }
+  p.maps_ready = ok;
+  return ok ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+namespace {
+
+template <int MODE, int BH>
+cudaError_t launch_gemm(const GemmParams &g, cudaStream_t s) {
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel<MODE, BH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Ring<BH>::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    configured_dev = dev;
+  }
+  const int grid = sm_count() & ~1;  // CTA pairs
+  grouped_gemm_kernel<MODE, BH><<<grid, kGemmThreads, Ring<BH>::kSmemBytes, s>>>(g);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
+                       cudaStream_t s, int *launches) {
+  GemmParams g{};
+  g.group_off = group_off;
+  g.tile_off = tile_off;
+  g.tile_n = p.tile_n;
+  g.q_begin = p.q_begin;
+  g.q_end = p.q_end;
+  const bool decode = p.tile_n <= 64;
+
+  // gate + up -> h: per replica A rows [gate d_e | up d_e]; 128 features per tile
+  g.tm_a = p.tm_w13;
+  for (int i = 0; i < 5; ++i) g.tm_b[i] = p.tm_xp[i];
+  g.K = p.d_h;
+  g.m_tiles = p.d_e / 128;
+  g.m_per_q = 2 * p.d_e;
+  g.up_off = p.d_e;
+  g.out = reinterpret_cast<__nv_bfloat16 *>(p.h);
+  g.out_ld = p.d_e;
+  cudaError_t err = decode ? launch_gemm<kSwiglu, 32>(g, s) : launch_gemm<kSwiglu, 128>(g, s);
+  if (err != cudaSuccess) return err;
+
+  // down: y = h Wd^T, 256 output features per tile
+  g.tm_a = p.tm_w2;
+  for (int i = 0; i < 5; ++i) g.tm_b[i] = p.tm_h[i];
+  g.K = p.d_e;
+  g.m_tiles = p.d_h / 256;
+  g.m_per_q = p.d_h;
+  g.up_off = 0;
+  g.out = reinterpret_cast<__nv_bfloat16 *>(p.y);
+  g.out_ld = p.d_h;
+  err = decode ? launch_gemm<kPlain, 32>(g, s) : launch_gemm<kPlain, 128>(g, s);
+  if (launches) *launches += 2;
+  return err;
+}
+
+}  // namespace janus

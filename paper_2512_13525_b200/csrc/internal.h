@@ -28,7 +28,8 @@ struct SchedArgs {
   int policy;
   uint64_t rng_state;  // derive_seed(seed, "sched/random")
   janus_assignment out;
-  int32_t *tile_off;   // [R+1] n-tile prefix for the grouped GEMM (BN = kTileN), optional
+  int32_t *tile_off;   // [R+1] n-tile prefix for the grouped GEMM, optional
+  int tile_n;          // token rows per GEMM n-tile (64 or 256)
   uint64_t *trace;     // [7] phase timestamps (%globaltimer), optional
   int id_bits;         // bits of the largest expert id (ballot-based peer matching)
 };
@@ -44,15 +45,16 @@ cudaError_t launch_schedule(const SchedArgs &a, cudaStream_t stream);
 size_t schedule_smem_bytes(int E, int N, int R);
 
 // MoE FFN workspace (ffn.cu).
-constexpr int kTileN = 128;  // token rows per GEMM tile (UMMA N <= 128)
+constexpr int kTileN = 256;  // token rows per GEMM tile (CTA-pair UMMA N <= 256)
 
 struct FfnPlan {
   int d_h = 0, d_e = 0, S_alloc = 0;
   int q_begin = 0, q_end = 0;   // replica groups computed here
+  int tile_n = kTileN;          // token rows per n-tile for this call (64 decode / 256)
   const void *w13 = nullptr, *w2 = nullptr;
   void *xp = nullptr, *h = nullptr, *y = nullptr;  // bf16 [S_alloc][.]
   CUtensorMap tm_w13, tm_w2;
-  CUtensorMap tm_xp[4], tm_h[4];  // box rows 16/32/64/128
+  CUtensorMap tm_xp[5], tm_h[5];  // box rows 8/16/32/64/128 (half of a pair's N)
   bool maps_ready = false;
 };
 
@@ -125,6 +127,25 @@ struct janus_ctx {
   void *d_x = nullptr, *d_outbuf = nullptr;
   int32_t *d_experts = nullptr;
   float *d_gw = nullptr;
+
+  // CUDA-graph replay of the single-GPU layer (janus_moe_layer_async)
+  struct GraphKey {
+    const void *x, *experts, *gw, *out;
+    int T;
+    bool operator==(const GraphKey &o) const {
+      return x == o.x && experts == o.experts && gw == o.gw && out == o.out && T == o.T;
+    }
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    uint64_t kernels;  // kernel nodes in the graph
+    uint64_t last_use;
+  };
+  bool use_graph = true;
+  cudaStream_t cap_stream = nullptr;
+  std::vector<GraphEntry> graphs;  // small LRU cache (a serving loop rotates few buffers)
+  uint64_t graph_clock = 0;
 
   // attention <-> MoE exchange
   bool xfer_ready = false;
