@@ -11,85 +11,144 @@ namespace janus {
 namespace {
 
 // ------------------------------------------------------------ permute -----
-// xp[slot_row[s]] = x[s / k] for the slots routed to `instance` (all slots
-// when instance < 0).  Slot-major: reads of x are sequential and every row
-// write is a contiguous burst.  One thread per 16-B chunk; grid-stride.
+// xp[slot_row[t*k+j]] = x[t] for the slots routed to `instance` (all slots
+// when instance < 0).  Token-major: one warp task = one 32*U-chunk segment of
+// token t's row, loaded once into registers and stored to each of the token's
+// k destination rows (x is read once; the k row indices are loaded by lanes
+// j < k and broadcast with shuffles).
 // (A TMA tile::gather4 fusion of this copy into the GEMM's B loads was
 // measured at ~16 cycles per gathered 128-B row per SM — 2x slower at T=4096 —
-// see profiles/README.md.)
+// and a cp.async gather broke even at best; see profiles/README.md.)
+// volatile so the 8 x U loads of a combine group stay ahead of their uses
+__device__ __forceinline__ uint4 ld_nc(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+constexpr int kPermU = 4;    // 16-B chunks per lane per task (2 KB segments)
+constexpr int kCombU = 2;    // 16-B chunks per lane per task (1 KB segments)
+constexpr int kWarpsPerBlock = 4;
+
 __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__restrict__ slot_row,
-                               const int32_t *__restrict__ slot_inst, int instance, int S, int k,
-                               int vec_per_row, uint4 *__restrict__ xp) {
-  const long long n = (long long)S * vec_per_row;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int s = (int)(i / vec_per_row), c = (int)(i % vec_per_row);
-    if (instance >= 0 && __ldg(slot_inst + s) != instance) continue;
-    xp[(size_t)__ldg(slot_row + s) * vec_per_row + c] = __ldg(x + (size_t)(s / k) * vec_per_row + c);
+                               const int32_t *__restrict__ slot_inst, int instance, int T, int k,
+                               int vec, uint4 *__restrict__ xp) {
+  const int lane = threadIdx.x & 31;
+  const int segs = (vec + 32 * kPermU - 1) / (32 * kPermU);
+  const int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (task >= T * segs) return;
+  const int t = task / segs, c0 = (task % segs) * 32 * kPermU + lane;
+  const uint4 *src = x + (size_t)t * vec;
+  uint4 v[kPermU];
+#pragma unroll
+  for (int u = 0; u < kPermU; ++u) {
+    const int c = c0 + 32 * u;
+    if (c < vec) v[u] = __ldg(src + c);
+  }
+  for (int j0 = 0; j0 < k; j0 += 32) {
+    const int j = j0 + lane;
+    int row = -1;
+    if (j < k) {
+      const int s = t * k + j;
+      if (instance < 0 || __ldg(slot_inst + s) == instance) row = __ldg(slot_row + s);
+    }
+    const int n = min(32, k - j0);
+    for (int jj = 0; jj < n; ++jj) {
+      const int r = __shfl_sync(0xffffffffu, row, jj);
+      if (r < 0) continue;
+      uint4 *dst = xp + (size_t)r * vec;
+#pragma unroll
+      for (int u = 0; u < kPermU; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < vec) dst[c] = v[u];
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------ combine -----
 // out[t] = sum_j w[t,j] * y[slot_row[t,j]] over the slots routed to `instance`
-// (all slots when instance < 0), j ascending, fp32, then bf16.
-__global__ void combine_kernel(const __nv_bfloat16 *__restrict__ y,
-                               const int32_t *__restrict__ slot_row,
-                               const int32_t *__restrict__ slot_inst, int instance,
-                               const float *__restrict__ gw, int T, int k, int d_h,
-                               __nv_bfloat16 *__restrict__ out) {
-  // One thread per (token, 16-B output chunk); the k row loads of a chunk are
-  // issued together (groups of 8) before any is consumed.
-  const int vec = d_h / 8;
-  const long long n = (long long)T * vec;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int t = (int)(idx / vec), c = (int)(idx % vec);
-    float acc[8];
+// (all slots when instance < 0), j ascending, fp32, then bf16.  One warp task
+// = one 32*U-chunk segment of token t; the row indices / weights are loaded by
+// lanes j < k and broadcast; 8 rows x U chunks are in flight per lane.
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
+    combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
+                   const int32_t *__restrict__ slot_inst, int instance,
+                   const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int segs = (vec + 32 * kCombU - 1) / (32 * kCombU);
+  const int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (task >= T * segs) return;
+  const int t = task / segs, c0 = (task % segs) * 32 * kCombU + lane;
+  float acc[kCombU][8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-    for (int j0 = 0; j0 < k; j0 += 8) {
-      uint4 v[8];
-      float w[8];
+  for (int u = 0; u < kCombU; ++u)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u;
-        w[u] = 0.f;
-        v[u] = make_uint4(0, 0, 0, 0);
-        if (j < k) {
-          const int s = t * k + j;
-          if (instance < 0 || __ldg(slot_inst + s) == instance) {
-            w[u] = __ldg(gw + s);
-            v[u] = __ldg(reinterpret_cast<const uint4 *>(y + (size_t)__ldg(slot_row + s) * d_h) + c);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {  // fixed j order: bitwise reproducible
-        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v[u]);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h[e]);
-          acc[2 * e] += w[u] * f.x;
-          acc[2 * e + 1] += w[u] * f.y;
-        }
+    for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+  for (int j0 = 0; j0 < k; j0 += 32) {
+    const int j = j0 + lane;
+    int row = -1;
+    float w = 0.f;
+    if (j < k) {
+      const int s = t * k + j;
+      if (instance < 0 || __ldg(slot_inst + s) == instance) {
+        row = __ldg(slot_row + s);
+        w = __ldg(gw + s);
       }
     }
+    const int n = min(32, k - j0);
+    for (int jj = 0; jj < n; jj += 8) {
+      uint4 v[8][kCombU];
+      float wv[8];
+      const uint4 *src[8];
+      bool ok[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int r = __shfl_sync(0xffffffffu, row, (jj + b) & 31);
+        const float wb = __shfl_sync(0xffffffffu, w, (jj + b) & 31);
+        ok[b] = jj + b < n && r >= 0;
+        wv[b] = ok[b] ? wb : 0.f;
+        src[b] = y + (size_t)(ok[b] ? r : 0) * vec;  // clamped; masked below
+      }
+      // all 8 x U loads are issued before the first is consumed
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int u = 0; u < kCombU; ++u) {
+          const int c = c0 + 32 * u;
+          v[b][u] = ld_nc(src[b] + min(c, vec - 1));
+        }
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int u = 0; u < kCombU; ++u)
+          if (!ok[b] || c0 + 32 * u >= vec) v[b][u] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int b = 0; b < 8; ++b)  // fixed j order: bitwise reproducible
+#pragma unroll
+        for (int u = 0; u < kCombU; ++u) {
+          const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v[b][u]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            acc[u][2 * e] += wv[b] * f.x;
+            acc[u][2 * e + 1] += wv[b] * f.y;
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kCombU; ++u) {
+    const int c = c0 + 32 * u;
+    if (c >= vec) continue;
     uint4 o;
     __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
-    reinterpret_cast<uint4 *>(out + (size_t)t * d_h)[c] = o;
+    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(acc[u][2 * e], acc[u][2 * e + 1]);
+    out[(size_t)t * vec + c] = o;
   }
-}
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
 }
 
 }  // namespace
@@ -97,11 +156,12 @@ int sm_count() {
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, int S, int k, int d_h, void *xp, cudaStream_t s) {
   if (S == 0) return cudaSuccess;
-  const long long threads = (long long)S * (d_h / 8);
-  const int blocks = (int)std::min<long long>((threads + 255) / 256, sm_count() * 16);
-  permute_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4 *>(x), slot_row,
-                                        slot_instance, instance, S, k, d_h / 8,
-                                        reinterpret_cast<uint4 *>(xp));
+  const int T = S / k, vec = d_h / 8;
+  const int tasks = T * ((vec + 32 * kPermU - 1) / (32 * kPermU));
+  const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  permute_kernel<<<blocks, 32 * kWarpsPerBlock, 0, s>>>(reinterpret_cast<const uint4 *>(x),
+                                                        slot_row, slot_instance, instance, T, k,
+                                                        vec, reinterpret_cast<uint4 *>(xp));
   return cudaGetLastError();
 }
 
@@ -109,11 +169,12 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
                            cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  const long long threads = (long long)T * (d_h / 8);
-  const int blocks = (int)std::min<long long>((threads + 255) / 256, sm_count() * 16);
-  combine_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16 *>(y), slot_row,
-                                        slot_instance, instance, gate_w, T, k, d_h,
-                                        reinterpret_cast<__nv_bfloat16 *>(out));
+  const int vec = d_h / 8;
+  const int tasks = T * ((vec + 32 * kCombU - 1) / (32 * kCombU));
+  const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  combine_kernel<<<blocks, 32 * kWarpsPerBlock, 0, s>>>(reinterpret_cast<const uint4 *>(y),
+                                                        slot_row, slot_instance, instance, gate_w,
+                                                        T, k, vec, reinterpret_cast<uint4 *>(out));
   return cudaGetLastError();
 }
 
