@@ -147,6 +147,7 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->ffn.xp);
   dfree(ctx->ffn.h);
   dfree(ctx->ffn.y);
+  dfree(ctx->ffn.tile_ctr);
   dfree(ctx->d_x);
   dfree(ctx->d_outbuf);
   dfree(ctx->d_experts);
@@ -408,6 +409,8 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   dfree(ctx->ffn.xp);
   dfree(ctx->ffn.h);
   dfree(ctx->ffn.y);
+  dfree(ctx->ffn.tile_ctr);
+  ctx->ffn.tile_ctr = nullptr;
   free_assign(ctx->ws);
   dfree(ctx->ws_tile_off);
   dfree(ctx->d_x);
@@ -425,6 +428,8 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   CK(cudaMalloc(&ctx->ffn.y, (size_t)S_alloc * d_h * 2));
   CK(cudaMemset(ctx->ffn.xp, 0, (size_t)S_alloc * d_h * 2));
   CK(cudaMemset(ctx->ffn.h, 0, (size_t)S_alloc * d_e * 2));
+  CK(dalloc(&ctx->ffn.tile_ctr, 4));
+  CK(cudaMemset(ctx->ffn.tile_ctr, 0, 4 * sizeof(unsigned)));
   CK(alloc_assign(ctx->ws, S, m.E, m.N, m.R));
   CK(dalloc(&ctx->ws_tile_off, m.R + 1));
   CK(cudaMalloc(&ctx->d_x, (size_t)max_tokens * d_h * 2));

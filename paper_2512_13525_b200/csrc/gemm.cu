@@ -23,11 +23,14 @@
 // Per CTA: warp 0 TMA producer, warp 1 TMEM owner (+ the MMA issuer in the
 // leader CTA), warps 2-5 epilogue (tcgen05.ld -> math -> bf16 -> smem ->
 // coalesced 16-B stores).  6-stage smem ring, 2 TMEM accumulators of 256
-// columns.  Persistent: 74 pairs walk the tile list that the scheduler kernel
-// wrote to device memory (group_off, tile_off) — no host sync.
+// columns.  Persistent: 74 pairs draw tiles from a global counter (dynamic
+// scheduling: a pair that drew a cheap tile draws the next one sooner) over the
+// tile list that the scheduler kernel wrote to device memory (group_off,
+// tile_off) — no host sync.
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -37,10 +40,13 @@ namespace {
 constexpr int kBK = 64;                        // K elements per stage (128-B rows, SW128)
 constexpr int kATileBytes = 128 * kBK * 2;     // 16 KB: this CTA's 128 weight rows
 constexpr int kEpiCols = 32;                   // token columns per epilogue chunk
-constexpr int kStagingBytes = kEpiCols * 128 * 2;     // 32 rows x 128 bf16
-constexpr int kXchgBytes = 128 * (kEpiCols + 1) * 4;  // SwiGLU exchange, padded rows
-constexpr int kGemmThreads = 192;
+constexpr int kEpiGroups = 2;                  // epilogue warpgroups (alternate 32-column chunks)
+constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kWarpStaging = kEpiCols * 32 * 2;  // per epilogue warp: 32 tokens x <=32 features bf16
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps + 32;  // + the B-producer warp
 constexpr int kTmemCols = 512;                 // 2 accumulators x 256 columns
+constexpr int kTQ = 4;                         // tile-queue slots (dynamic tile scheduler)
+constexpr int kTQConsumers = 4 + 2 * kEpiWarps;  // leader MMA, peer A producer, 2 B producers, epilogue
 
 // Two shapes of the smem ring, chosen per launch from the expected rows per
 // replica group (api.cu): BH = token rows per CTA per tile (pair N = 2*BH).
@@ -52,16 +58,19 @@ struct Ring {
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
   static constexpr int kStages = BH == 128 ? 6 : 9;
   static constexpr int kSmemBytes =
-      kStages * kStageBytes + kStagingBytes + kXchgBytes + 1024 /*align*/ + 256 /*barriers*/;
+      kStages * kStageBytes + kEpiWarps * kWarpStaging + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 enum Mode { kSwiglu = 0, kPlain = 1 };
 
 struct GemmParams {
-  CUtensorMap tm_a;     // weights [Q*M_per_q][K]; box 64 rows (SWIGLU) / 128 rows (PLAIN)
+  CUtensorMap tm_a;     // weights; SWIGLU: 4-D gate/up interleave map (box = 128 rows), PLAIN: 2-D, box 128 rows
   CUtensorMap tm_b[5];  // activations [S_alloc][K], box rows 8/16/32/64/128 (= N/2)
   const int32_t *group_off;
   const int32_t *tile_off;  // n-tiles of tile_n rows per group (prefix)
+  unsigned *ctr;            // [2] next-tile counter, finished CTAs (reset by the last CTA)
+  int order;                // tile order: 0 group-major, 1 zig-zag
+  int dbg;
   int tile_n;     // token rows per tile (= 2*BH)
   int q_begin, q_end;
   int K;          // reduction length
@@ -99,6 +108,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// Publish a 32-bit value into a CTA's smem and complete that CTA's mbarrier
+// phase with it (arrive + expect 4 bytes, then st.async completing them): no
+// release fence, so the issuing thread does not wait for its in-flight TMA.
+__device__ __forceinline__ void publish_u32(uint32_t cl_dst, uint32_t v, uint32_t cl_bar) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], 4;" ::"r"(
+                   cl_bar)
+               : "memory");
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   cl_dst),
+               "r"(v), "r"(cl_bar)
+               : "memory");
+}
+// Relaxed arrive (consumers of the tile queue: only "read before reuse").
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 // Arrive on an mbarrier in another CTA of the cluster (cluster-window address).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
@@ -124,6 +150,16 @@ __device__ __forceinline__ void tma_load_pair(void *dst, const CUtensorMap *tm, 
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar_leader), "l"(policy)
+      : "memory");
+}
+// 4-D variant (the SWIGLU weight map: {k, row in 8, gate/up, 8-row group}).
+__device__ __forceinline__ void tma_load_pair_4d(void *dst, const CUtensorMap *tm,
+                                                 uint32_t bar_leader, int x0, int x3,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x0), "r"(0), "r"(x3), "r"(bar_leader), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
@@ -189,8 +225,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+// 16 lanes x 256 bit, 4 repeats along columns: thread t gets, per repeat i,
+// lane (t/4) columns 8i + 2(t%4) + {0,1} in r[4i], r[4i+1] and lane (t/4)+8,
+// same columns, in r[4i+2], r[4i+3].
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 struct TileCoord {
@@ -203,7 +249,7 @@ struct TileCoord {
 // tiles with the cold groups' weight-streaming tiles: replica order follows
 // placement order, which is by descending load (experts.cpp place_replicas).
 __device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in, int total) {
-  const int t = (t_in & 1) ? total - 1 - (t_in >> 1) : (t_in >> 1);
+  const int t = !p.order ? t_in : (t_in & 1) ? total - 1 - (t_in >> 1) : (t_in >> 1);
   const int base = p.tile_off[p.q_begin];
   int lo = p.q_begin, hi = p.q_end;  // find q: (tile_off[q]-base)*m <= t < (tile_off[q+1]-base)*m
   while (hi - lo > 1) {
@@ -221,13 +267,10 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in, i
   c.r0 = p.group_off[q] + n * p.tile_n;
   c.rows = min(p.tile_n, p.group_off[q + 1] - c.r0);
   const int need = (c.rows + 1) / 2;  // rows per CTA
-  c.half = need <= 8 ? 8 : need <= 16 ? 16 : need <= 32 ? 32 : need <= 64 ? 64 : 128;
+  c.half = (need + 7) & ~7;  // UMMA N = 2*half: any multiple of 16 up to 256
   return c;
 }
 
-__device__ __forceinline__ int box_index(int half) {
-  return half == 8 ? 0 : half == 16 ? 1 : half == 32 ? 2 : half == 64 ? 3 : 4;
-}
 
 template <int MODE, int BH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
@@ -238,20 +281,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *stage_base = smem;
-  __nv_bfloat16 *staging = reinterpret_cast<__nv_bfloat16 *>(smem + kStages * kStageBytes);
-  float *xchg = reinterpret_cast<float *>(smem + kStages * kStageBytes + kStagingBytes);
-  uint64_t *bars =
-      reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes + kStagingBytes + kXchgBytes);
+  unsigned char *epi_base = smem + kStages * kStageBytes;  // per epilogue warp: staging
+  uint64_t *bars = reinterpret_cast<uint64_t *>(epi_base + kEpiWarps * kWarpStaging);
   uint64_t *full = bars;                      // [kStages] leader: TMA bytes of both CTAs
   uint64_t *empty = bars + kStages;           // [kStages] both: MMA done with the stage
   uint64_t *tfull = bars + 2 * kStages;       // [2]       both: accumulator ready
   uint64_t *tempty = bars + 2 * kStages + 2;  // [2]       leader: both epilogues drained it
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 2 * kStages + 4);
+  uint64_t *tq_full = bars + 2 * kStages + 4;  // [kTQ]   both: tile index published
+  uint64_t *tq_empty = tq_full + kTQ;          // [kTQ]   leader: every consumer read it
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tq_empty + kTQ);
+  volatile int *tq = reinterpret_cast<volatile int *>(tmem_holder + 4);  // [kTQ]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
   const bool leader = crank == 0;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int total = (p.tile_off[p.q_end] - p.tile_off[p.q_begin]) * p.m_tiles;
   const int kblocks = p.K / kBK;
 
@@ -264,7 +307,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[s], 2 * kEpiWarps);  // epilogue warps of both CTAs
+    }
+    for (int s = 0; s < kTQ; ++s) {
+      mbar_init(&tq_full[s], 1);
+      mbar_init(&tq_empty[s], kTQConsumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -279,38 +326,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // Dynamic tile scheduler: the leader's producer takes tile indices from a
+  // global counter (one tile ahead) and publishes each through a kTQ-slot
+  // queue in both CTAs' smem; the other roles of the pair read them from
+  // there.  Pairs that draw cheap tiles draw more of them.
   if (warp == 0) {
-    // ===================== TMA producer (both CTAs) =====================
+    // ============ weight (A) producer + tile fetch (both CTAs) ============
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();  // weights: streamed once
-      const uint64_t pol_x = policy_evict_last();   // token rows: reused by every m-block
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < total; t += npairs) {
+      int slot = 0;
+      uint32_t tq_phase = 0;
+      int t = leader ? (int)atomicAdd(p.ctr, 1u) : 0;
+      while (true) {
+        if (leader) {
+          mbar_wait(&tq_empty[slot], tq_phase ^ 1);
+          const uint32_t dst = smem_u32((const void *)&tq[slot]), bar = smem_u32(&tq_full[slot]);
+          publish_u32(mapa(dst, 0), (uint32_t)t, mapa(bar, 0));
+          publish_u32(mapa(dst, 1), (uint32_t)t, mapa(bar, 1));
+        } else {
+          mbar_wait(&tq_full[slot], tq_phase);
+          t = tq[slot];
+          mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
+        }
+        if (++slot == kTQ) {
+          slot = 0;
+          tq_phase ^= 1;
+        }
+        if (t >= total) break;
+        const int t_next = leader ? (int)atomicAdd(p.ctr, 1u) : 0;  // consumed after this tile
         const TileCoord c = tile_coord(p, t, total);
-        const int bi = box_index(c.half);
-        const uint32_t bytes_pair = 2u * (kATileBytes + (uint32_t)c.half * kBK * 2);
+        const uint32_t bytes_pair = 2u * (kATileBytes + ((p.dbg & 2) ? 0u : (uint32_t)c.half * kBK * 2));
         const int rowq = (c.q - p.q_begin) * p.m_per_q;
-        const int brow = c.r0 + (int)crank * c.half;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char *sa = stage_base + stage * kStageBytes;
           const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
-          if (leader) mbar_expect_tx(&full[stage], bytes_pair);
+          if (leader) mbar_expect_tx(&full[stage], bytes_pair);  // A and B bytes of both CTAs
           if (MODE == kSwiglu) {
-            const int f0 = c.m * 128 + (int)crank * 64;  // this CTA's 64 features
-            tma_load_pair(sa, &p.tm_a, bar, kb * kBK, rowq + f0, pol_w);
-            tma_load_pair(sa + kATileBytes / 2, &p.tm_a, bar, kb * kBK, rowq + p.up_off + f0,
-                          pol_w);
+            // this CTA's 64 features as 8 blocks of (8 gate rows, 8 up rows)
+            const int f0 = c.m * 128 + (int)crank * 64;
+            tma_load_pair_4d(sa, &p.tm_a, bar, kb * kBK, (rowq + f0) >> 3, pol_w);
           } else {
             tma_load_pair(sa, &p.tm_a, bar, kb * kBK, rowq + c.m * 256 + (int)crank * 128, pol_w);
           }
-          tma_load_pair(sa + kATileBytes, &p.tm_b[bi], bar, kb * kBK, brow, pol_x);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
+        t = t_next;
       }
     }
   } else if (warp == 1) {
@@ -320,7 +386,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair; t < total; t += npairs) {
+      int slot = 0;
+      uint32_t tq_phase = 0;
+      while (true) {
+        mbar_wait(&tq_full[slot], tq_phase);
+        const int t = tq[slot];
+        mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
+        if (++slot == kTQ) {
+          slot = 0;
+          tq_phase ^= 1;
+        }
+        if (t >= total) break;
         const TileCoord c = tile_coord(p, t, total);
         const uint32_t idesc = idesc_bf16_m256(2 * c.half);
         const uint32_t d = tmem_base + acc * 256;
@@ -347,73 +423,135 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
+  } else if (warp == 2 + kEpiWarps) {
+    // ============ token-row (B) producer (both CTAs) ============
+    // A separate thread from the weight producer: the per-k-block TMA issue
+    // cost of one thread was measurable on the critical path.
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_last();  // token rows: reused by every m-block
+      int stage = 0;
+      uint32_t phase = 0;
+      int slot = 0;
+      uint32_t tq_phase = 0;
+      while (true) {
+        mbar_wait(&tq_full[slot], tq_phase);
+        const int t = tq[slot];
+        mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
+        if (++slot == kTQ) {
+          slot = 0;
+          tq_phase ^= 1;
+        }
+        if (t >= total) break;
+        const TileCoord c = tile_coord(p, t, total);
+        const int brow = c.r0 + (int)crank * c.half;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char *sb = stage_base + stage * kStageBytes + kATileBytes;
+          const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
+          if (!(p.dbg & 2)) {
+            // half = 8*m rows: one TMA box per set bit of m, largest first (boxes
+            // of 128/64/32/16/8 rows land on 8-row = 1024-B swizzle atoms)
+            int off = 0;
+#pragma unroll 1
+            for (int m8 = c.half >> 3; m8;) {
+              const int i = 31 - __clz(m8);
+              tma_load_pair(sb + off * 128, &p.tm_b[i], bar, kb * kBK, brow + off, pol_x);
+              off += 8 << i;
+              m8 ^= 1 << i;
+            }
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
   } else {
-    // ===================== epilogue (warps 2..5, both CTAs) =====================
-    const int quad = warp & 3;        // TMEM lanes quad*32 .. +31
-    const int et = threadIdx.x - 64;  // 0..127
+    // ============ epilogue (warps 2.., both CTAs) ============
+    // Warp w drains TMEM lanes 32*(w%4).. +31 of the 32-column chunks grp,
+    // grp + kEpiGroups, ... of each accumulator (grp = (w-2)/4): two warps per
+    // SM sub-partition hide each other's tcgen05.ld / store latency, and each
+    // warp transposes through its own smem (no cross-warp barrier).
+    const int quad = warp & 3;  // TMEM lane quarter (warp % 4 rule)
+    const int grp = (warp - 2) >> 2;
+    __nv_bfloat16 *stg = reinterpret_cast<__nv_bfloat16 *>(epi_base + (warp - 2) * kWarpStaging);
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa(smem_u32(&tempty[1]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair; t < total; t += npairs) {
+    int slot = 0;
+    uint32_t tq_phase = 0;
+    while (true) {
+      mbar_wait(&tq_full[slot], tq_phase);
+      const int t = tq[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
+      if (++slot == kTQ) {
+        slot = 0;
+        tq_phase ^= 1;
+      }
+      if (t >= total) break;
       const TileCoord c = tile_coord(p, t, total);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t d = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
       // accumulator column j <-> token row r0 + j (CTA 0 loaded rows [0, half),
       // CTA 1 rows [half, 2*half) of the tile)
-      for (int c0 = 0; c0 < c.rows; c0 += kEpiCols) {
+      for (int c0 = grp * kEpiCols; c0 < ((p.dbg & 1) ? 0 : c.rows); c0 += kEpiGroups * kEpiCols) {
         const int rows = min(kEpiCols, c.rows - c0);
-        float v[32];
         if (MODE == kSwiglu) {
-          // lanes 0..63 hold the gate projection, lanes 64..127 the up
-          // projection of the same 64 features: every warp parks its rows in
-          // smem, then all 128 threads each finish 16 (feature, column) pairs.
-          tmem_ld32(d + c0, v);
-          {
-            float *xr = xchg + (quad * 32 + lane) * (kEpiCols + 1);
+          // TMEM lanes 16b..16b+7 hold the gate rows and 16b+8..16b+15 the up
+          // rows of CTA-local features 8b..8b+7 (the 4-D weight map's
+          // interleave).  The 16x256b shape gives each thread gate and up of
+          // one feature for two adjacent columns per 8-column repeat, so
+          // silu(g)*u is formed in registers.  This warp: features 16*quad..+15.
+          const int fq = lane >> 2, cq = 2 * (lane & 3);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) xr[j] = v[j];
-          }
-          named_bar(1, 128);
-          {
-            const int f = et & 63, j0 = (et >> 6) * 16;
-            const float *gr = xchg + f * (kEpiCols + 1);
-            const float *ur = xchg + (64 + f) * (kEpiCols + 1);
+          for (int bb = 0; bb < 2; ++bb) {
+            uint32_t r[16];
+            tmem_ld_16x256b_x4(d + ((uint32_t)(16 * bb) << 16) + c0, r);
+            const int f = 8 * bb + fq;
 #pragma unroll
-            for (int j = j0; j < j0 + 16; ++j) {
-              const float g = gr[j];
-              staging[j * 64 + f] = __float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * ur[j]);
-            }
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const float g = __uint_as_float(r[4 * i + e]), u = __uint_as_float(r[4 * i + 2 + e]);
+                stg[(8 * i + cq + e) * 16 + f] =
+                    __float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u);
+              }
           }
-          named_bar(1, 128);
-          __nv_bfloat16 *obase =
-              p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 128 + (int)crank * 64;
-          for (int i = et; i < rows * 8; i += 128) {  // 64 features = 8 x 16 B per row
-            const int r = i >> 3, ch = i & 7;
-            *reinterpret_cast<uint4 *>(obase + (size_t)r * p.out_ld + ch * 8) =
-                *reinterpret_cast<const uint4 *>(staging + r * 64 + ch * 8);
+          __syncwarp();
+          __nv_bfloat16 *obase = p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 128 +
+                                 (int)crank * 64 + quad * 16;
+          for (int i = lane; i < rows * 2; i += 32) {  // 16 features = 2 x 16 B per row
+            const int rr = i >> 1, ch = i & 1;
+            *reinterpret_cast<uint4 *>(obase + (size_t)rr * p.out_ld + ch * 8) =
+                *reinterpret_cast<const uint4 *>(stg + rr * 16 + ch * 8);
           }
-          named_bar(1, 128);
+          __syncwarp();
         } else {
+          float v[32];
           tmem_ld32(d + c0, v);
-          const int f = quad * 32 + lane;  // 0..127
 #pragma unroll
-          for (int j = 0; j < 32; ++j) staging[j * 128 + f] = __float2bfloat16_rn(v[j]);
-          named_bar(1, 128);
-          __nv_bfloat16 *obase =
-              p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 256 + (int)crank * 128;
-          for (int i = et; i < rows * 16; i += 128) {  // 128 features = 16 x 16 B per row
-            const int r = i >> 4, ch = i & 15;
-            *reinterpret_cast<uint4 *>(obase + (size_t)r * p.out_ld + ch * 8) =
-                *reinterpret_cast<const uint4 *>(staging + r * 128 + ch * 8);
+          for (int j = 0; j < 32; ++j) stg[j * 32 + lane] = __float2bfloat16_rn(v[j]);
+          __syncwarp();
+          __nv_bfloat16 *obase = p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 256 +
+                                 (int)crank * 128 + quad * 32;
+          for (int i = lane; i < rows * 4; i += 32) {  // 32 features = 4 x 16 B per row
+            const int rr = i >> 2, ch = i & 3;
+            *reinterpret_cast<uint4 *>(obase + (size_t)rr * p.out_ld + ch * 8) =
+                *reinterpret_cast<const uint4 *>(stg + rr * 32 + ch * 8);
           }
-          named_bar(1, 128);
+          __syncwarp();
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      // relaxed: only the TMEM reads (complete: tcgen05.wait::ld, fenced
+      // above) must precede the MMA's reuse of the accumulator; a release
+      // arrive would also wait for this warp's global stores to be acked
+      if (lane == 0) mbar_arrive_cluster_relaxed(acc ? tempty_leader1 : tempty_leader0);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -422,6 +560,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
   tc_fence_before();
   cluster_sync_all();
+  if (threadIdx.x == 0) {  // the last CTA to finish resets the tile counter for the next launch
+    __threadfence();
+    if (atomicAdd(p.ctr + 1, 1u) == gridDim.x - 1) {
+      atomicExch(p.ctr, 0u);
+      atomicExch(p.ctr + 1, 0u);
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -471,11 +616,27 @@ bool make_map(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t cols, u
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The gate/up weight store [Q][gate d_e | up d_e][d_h] as a 4-D map {k, row in
+// an 8-row block, gate/up (+d_e rows), 8-row block}: one box {64, 8, 2, 8}
+// lands as 8 x (8 gate rows, the 8 up rows of the same features) — the row
+// order the SwiGLU epilogue's 16x256b TMEM loads pair up.
+bool make_w13_map(CUtensorMap *tm, const void *base, uint64_t Q, uint64_t d_e, uint64_t d_h) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {d_h, 8, 2, (Q * 2 * d_e - d_e) / 8};
+  cuuint64_t strides[3] = {d_h * 2, d_e * d_h * 2, 8 * d_h * 2};
+  cuuint32_t box[4] = {64, 8, 2, 8};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 cudaError_t build_ffn_tensor_maps(FfnPlan &p) {
   const int Q = p.q_end - p.q_begin;
-  bool ok = make_map(&p.tm_w13, p.w13, (uint64_t)Q * 2 * p.d_e, p.d_h, 64) &&
+  bool ok = make_w13_map(&p.tm_w13, p.w13, Q, p.d_e, p.d_h) &&
             make_map(&p.tm_w2, p.w2, (uint64_t)Q * p.d_h, p.d_e, 128);
   for (int i = 0; i < 5 && ok; ++i) {
     ok = make_map(&p.tm_xp[i], p.xp, p.S_alloc, p.d_h, 8u << i) &&
@@ -512,6 +673,17 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   g.group_off = group_off;
   g.tile_off = tile_off;
   g.tile_n = p.tile_n;
+  static const int order = [] {
+    const char *e = getenv("JANUS_TILE_ORDER");
+    return e ? atoi(e) : 1;
+  }();
+  g.order = order;
+  static const int dbg = [] {
+    const char *e = getenv("JANUS_GEMM_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  g.dbg = dbg;
+  g.ctr = p.tile_ctr;
   g.q_begin = p.q_begin;
   g.q_end = p.q_end;
   const bool decode = p.tile_n <= 64;
@@ -531,6 +703,7 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   // down: y = h Wd^T, 256 output features per tile
   g.tm_a = p.tm_w2;
   for (int i = 0; i < 5; ++i) g.tm_b[i] = p.tm_h[i];
+  g.ctr = p.tile_ctr + 2;
   g.K = p.d_e;
   g.m_tiles = p.d_h / 256;
   g.m_per_q = p.d_h;

@@ -53,6 +53,7 @@ struct FfnPlan {
   int tile_n = kTileN;          // token rows per n-tile for this call (64 decode / 256)
   const void *w13 = nullptr, *w2 = nullptr;
   void *xp = nullptr, *h = nullptr, *y = nullptr;  // bf16 [S_alloc][.]
+  unsigned *tile_ctr = nullptr;  // [4] per GEMM: next-tile counter, finished CTAs (self-resetting)
   CUtensorMap tm_w13, tm_w2;
   CUtensorMap tm_xp[5], tm_h[5];  // box rows 8/16/32/64/128 (half of a pair's N)
   bool maps_ready = false;
