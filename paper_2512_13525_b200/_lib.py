@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libjanus_b200.so")
+LIB_PATH = os.environ.get("JANUS_LIB") or os.path.join(PKG, "libjanus_b200.so")  # override: A/B runs
 
 OK, EINVAL, EUNKNOWN_EXPERT, ECUDA, ESTATE, EUNSUPPORTED = range(6)
 POLICY_AEBS, POLICY_RANDOM = 0, 1

@@ -378,7 +378,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
       const int q = s_qidx[p];
       qof[e] = q;
       qcnt[q] = tot[e];
-      tcnt[q] = (tot[e] + a.tile_n - 1) / a.tile_n;
+      // tiles of tile_n rows; the last one also takes the remainder (gemm.cu)
+      tcnt[q] = a.merge_tail ? (tot[e] > 0 ? max(1, tot[e] / a.tile_n) : 0)
+                             : (tot[e] + a.tile_n - 1) / a.tile_n;
       atomicAdd(&routed[g], (unsigned)tot[e]);
     }
     if (leader) {

@@ -282,6 +282,10 @@ static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T
   a.out = out;
   a.tile_off = tile_off;
   a.tile_n = ctx->ffn.tile_n > 0 ? ctx->ffn.tile_n : janus::kTileN;
+  // decode tiles are weight-streaming bound: fold each group's remainder into
+  // its last tile (one pass over the weights); in the tensor regime the wide
+  // tile's halved weight prefetch depth costs more than it saves (measured)
+  a.merge_tail = a.tile_n <= 64;
   cudaError_t e = janus::launch_schedule(a, stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aebs_schedule_kernel");
   ctx->launches += 1;

@@ -69,7 +69,6 @@ struct GemmParams {
   const int32_t *group_off;
   const int32_t *tile_off;  // n-tiles of tile_n rows per group (prefix)
   unsigned *ctr;            // [2] next-tile counter, finished CTAs (reset by the last CTA)
-  int order;                // tile order: 0 group-major, 1 zig-zag
   int dbg;
   int tile_n;     // token rows per tile (= 2*BH)
   int q_begin, q_end;
@@ -119,6 +118,16 @@ __device__ __forceinline__ void publish_u32(uint32_t cl_dst, uint32_t v, uint32_
                    cl_dst),
                "r"(v), "r"(cl_bar)
                : "memory");
+}
+// One lane of a converged warp.  The single-thread roles (TMA producers, MMA
+// issuer) run as whole warps and issue through elect_one(), so their loop
+// state stays warp-uniform and ptxas keeps TMA/UMMA operands in uniform
+// registers (no per-instruction R2UR waterfall as under `if (lane == 0)`).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(pred));
+  return pred != 0;
 }
 // Relaxed arrive (consumers of the tile queue: only "read before reuse").
 __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
@@ -240,16 +249,20 @@ __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)
 }
 
 struct TileCoord {
-  int q, m, r0, rows, half;  // half = N/2 token rows loaded by each CTA
+  int q, m, r0, rows;
+  int half;     // token rows per CTA of the (first) sub-tile: UMMA N = 2*half
+  int half_hi;  // wide tiles: rows per CTA of the second sub-tile (rows tile_n..), else 0
 };
 
+__device__ __forceinline__ int rows_per_cta(int rows) { return (((rows + 1) >> 1) + 7) & ~7; }
+
 // Tile t (relative to the first tile of q_begin) -> (group, m-block, rows).
-// The list is walked zig-zag (t even: from the front, odd: from the back) so
-// that the pairs running at the same moment mix the hot groups' tensor-bound
-// tiles with the cold groups' weight-streaming tiles: replica order follows
-// placement order, which is by descending load (experts.cpp place_replicas).
-__device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in, int total) {
-  const int t = !p.order ? t_in : (t_in & 1) ? total - 1 - (t_in >> 1) : (t_in >> 1);
+// Group-major, n-tiles fastest (consecutive tiles share the weight block).  A
+// group of r rows has max(1, r / tile_n) tiles; the last one also takes the
+// remainder, so it can hold up to 2*tile_n - 1 rows ("wide": two sub-tiles
+// that share every weight k-block) — a remainder never costs its own pass over
+// the weights.
+__device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t) {
   const int base = p.tile_off[p.q_begin];
   int lo = p.q_begin, hi = p.q_end;  // find q: (tile_off[q]-base)*m <= t < (tile_off[q+1]-base)*m
   while (hi - lo > 1) {
@@ -265,12 +278,16 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in, i
   c.m = local / nt;
   const int n = local % nt;
   c.r0 = p.group_off[q] + n * p.tile_n;
-  c.rows = min(p.tile_n, p.group_off[q + 1] - c.r0);
-  const int need = (c.rows + 1) / 2;  // rows per CTA
-  c.half = (need + 7) & ~7;  // UMMA N = 2*half: any multiple of 16 up to 256
+  c.rows = n == nt - 1 ? p.group_off[q + 1] - c.r0 : p.tile_n;
+  if (c.rows > p.tile_n) {
+    c.half = p.tile_n >> 1;
+    c.half_hi = rows_per_cta(c.rows - p.tile_n);
+  } else {
+    c.half = rows_per_cta(c.rows);
+    c.half_hi = 0;
+  }
   return c;
 }
-
 
 template <int MODE, int BH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
@@ -332,37 +349,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   // there.  Pairs that draw cheap tiles draw more of them.
   if (warp == 0) {
     // ============ weight (A) producer + tile fetch (both CTAs) ============
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();  // weights: streamed once
-      int stage = 0;
-      uint32_t phase = 0;
-      int slot = 0;
-      uint32_t tq_phase = 0;
-      int t = leader ? (int)atomicAdd(p.ctr, 1u) : 0;
-      while (true) {
-        if (leader) {
-          mbar_wait(&tq_empty[slot], tq_phase ^ 1);
+    const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+    int stage = 0;
+    uint32_t phase = 0;
+    int slot = 0;
+    uint32_t tq_phase = 0;
+    int t = 0;
+    if (leader && lane == 0) t = (int)atomicAdd(p.ctr, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    while (true) {
+      if (leader) {
+        mbar_wait(&tq_empty[slot], tq_phase ^ 1);
+        if (elect_one()) {
           const uint32_t dst = smem_u32((const void *)&tq[slot]), bar = smem_u32(&tq_full[slot]);
           publish_u32(mapa(dst, 0), (uint32_t)t, mapa(bar, 0));
           publish_u32(mapa(dst, 1), (uint32_t)t, mapa(bar, 1));
-        } else {
-          mbar_wait(&tq_full[slot], tq_phase);
-          t = tq[slot];
-          mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
         }
-        if (++slot == kTQ) {
-          slot = 0;
-          tq_phase ^= 1;
-        }
-        if (t >= total) break;
-        const int t_next = leader ? (int)atomicAdd(p.ctr, 1u) : 0;  // consumed after this tile
-        const TileCoord c = tile_coord(p, t, total);
-        const uint32_t bytes_pair = 2u * (kATileBytes + ((p.dbg & 2) ? 0u : (uint32_t)c.half * kBK * 2));
-        const int rowq = (c.q - p.q_begin) * p.m_per_q;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          unsigned char *sa = stage_base + stage * kStageBytes;
-          const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
+        __syncwarp();
+      } else {
+        mbar_wait(&tq_full[slot], tq_phase);
+        t = tq[slot];
+        __syncwarp();
+        if (elect_one()) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
+      }
+      if (++slot == kTQ) {
+        slot = 0;
+        tq_phase ^= 1;
+      }
+      if (t >= total) break;
+      int t_next = 0;  // drawn one tile ahead; consumed after this tile
+      if (leader && lane == 0) t_next = (int)atomicAdd(p.ctr, 1u);
+      const TileCoord c = tile_coord(p, t);
+      const uint32_t bbytes = (p.dbg & 2) ? 0u : 2u * kBK * 2;  // per token row of the pair
+      const uint32_t bytes_pair = 2u * kATileBytes + bbytes * c.half;
+      const int rowq = (c.q - p.q_begin) * p.m_per_q;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char *sa = stage_base + stage * kStageBytes;
+        const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
+        if (elect_one()) {
           if (leader) mbar_expect_tx(&full[stage], bytes_pair);  // A and B bytes of both CTAs
           if (MODE == kSwiglu) {
             // this CTA's 64 features as 8 blocks of (8 gate rows, 8 up rows)
@@ -371,63 +396,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           } else {
             tma_load_pair(sa, &p.tm_a, bar, kb * kBK, rowq + c.m * 256 + (int)crank * 128, pol_w);
           }
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (c.half_hi) {  // wide tile: the next stage carries only the second sub-tile's B
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader && elect_one()) mbar_expect_tx(&full[stage], bbytes * c.half_hi);
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        t = t_next;
       }
+      t = __shfl_sync(0xffffffffu, t_next, 0);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
-    if (leader && lane == 0) {
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
+      uint32_t use = 0;  // accumulator uses so far: buffer use&1, phase (use>>1)&1
       int slot = 0;
       uint32_t tq_phase = 0;
       while (true) {
         mbar_wait(&tq_full[slot], tq_phase);
         const int t = tq[slot];
-        mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
+        __syncwarp();
+        if (elect_one()) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
         if (++slot == kTQ) {
           slot = 0;
           tq_phase ^= 1;
         }
         if (t >= total) break;
-        const TileCoord c = tile_coord(p, t, total);
+        const TileCoord c = tile_coord(p, t);
+        const bool wide = c.half_hi != 0;
         const uint32_t idesc = idesc_bf16_m256(2 * c.half);
-        const uint32_t d = tmem_base + acc * 256;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        const uint32_t idesc_hi = idesc_bf16_m256(wide ? 2 * c.half_hi : 16);
+        const uint32_t d = tmem_base + (use & 1) * 256, d_hi = tmem_base + ((use + 1) & 1) * 256;
+        mbar_wait(&tempty[use & 1], ((use >> 1) & 1) ^ 1);
+        if (wide) mbar_wait(&tempty[(use + 1) & 1], (((use + 1) >> 1) & 1) ^ 1);
         tc_fence_after();
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(stage_base + stage * kStageBytes);
-          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kATileBytes);
+        if (!wide) {
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(stage_base + stage * kStageBytes);
+            const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kATileBytes);
+            if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-          umma_commit_pair(&empty[stage]);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+              for (int k = 0; k < kBK / 16; ++k)
+                umma_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+              umma_commit_pair(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        } else {
+          // wide tile: stage s1 = weights + first sub-tile's rows, s2 = second
+          // sub-tile's rows; both sub-tiles reuse the weight k-block of s1
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            const int s1 = stage;
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            mbar_wait(&full[stage], phase);
+            const int s2 = stage;
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            tc_fence_after();
+            const uint32_t sa = smem_u32(stage_base + s1 * kStageBytes);
+            const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kATileBytes);
+            const uint64_t db2 = sw128_desc(smem_u32(stage_base + s2 * kStageBytes) + kATileBytes);
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)
+                umma_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)
+                umma_pair(d_hi, da + 2 * k, db2 + 2 * k, idesc_hi, (kb | k) != 0);
+              umma_commit_pair(&empty[s1]);
+              umma_commit_pair(&empty[s2]);
+            }
+            __syncwarp();
           }
         }
-        umma_commit_pair(&tfull[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+        if (elect_one()) {
+          umma_commit_pair(&tfull[use & 1]);
+          if (wide) umma_commit_pair(&tfull[(use + 1) & 1]);
         }
+        __syncwarp();
+        use += wide ? 2 : 1;
       }
     }
   } else if (warp == 2 + kEpiWarps) {
     // ============ token-row (B) producer (both CTAs) ============
-    // A separate thread from the weight producer: the per-k-block TMA issue
-    // cost of one thread was measurable on the critical path.
-    if (lane == 0) {
+    // A separate warp from the weight producer: the per-k-block TMA issue
+    // cost of one warp was measurable on the critical path.
+    {
       const uint64_t pol_x = policy_evict_last();  // token rows: reused by every m-block
       int stage = 0;
       uint32_t phase = 0;
@@ -436,33 +512,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       while (true) {
         mbar_wait(&tq_full[slot], tq_phase);
         const int t = tq[slot];
-        mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
+        __syncwarp();
+        if (elect_one()) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
         if (++slot == kTQ) {
           slot = 0;
           tq_phase ^= 1;
         }
         if (t >= total) break;
-        const TileCoord c = tile_coord(p, t, total);
-        const int brow = c.r0 + (int)crank * c.half;
+        const TileCoord c = tile_coord(p, t);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          unsigned char *sb = stage_base + stage * kStageBytes + kATileBytes;
-          const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
-          if (!(p.dbg & 2)) {
-            // half = 8*m rows: one TMA box per set bit of m, largest first (boxes
-            // of 128/64/32/16/8 rows land on 8-row = 1024-B swizzle atoms)
-            int off = 0;
+          for (int sub = 0; sub < (c.half_hi ? 2 : 1); ++sub) {
+            const int half = sub ? c.half_hi : c.half;
+            const int brow = c.r0 + sub * p.tile_n + (int)crank * half;
+            mbar_wait(&empty[stage], phase ^ 1);
+            unsigned char *sb = stage_base + stage * kStageBytes + kATileBytes;
+            const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
+            if (!(p.dbg & 2) && elect_one()) {
+              // half = 8*m rows: one TMA box per set bit of m, largest first (boxes
+              // of 128/64/32/16/8 rows land on 8-row = 1024-B swizzle atoms)
+              int off = 0;
 #pragma unroll 1
-            for (int m8 = c.half >> 3; m8;) {
-              const int i = 31 - __clz(m8);
-              tma_load_pair(sb + off * 128, &p.tm_b[i], bar, kb * kBK, brow + off, pol_x);
-              off += 8 << i;
-              m8 ^= 1 << i;
+              for (int m8 = half >> 3; m8;) {
+                const int i = 31 - __clz(m8);
+                tma_load_pair(sb + off * 128, &p.tm_b[i], bar, kb * kBK, brow + off, pol_x);
+                off += 8 << i;
+                m8 ^= 1 << i;
+              }
             }
-          }
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+            __syncwarp();
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -478,8 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     __nv_bfloat16 *stg = reinterpret_cast<__nv_bfloat16 *>(epi_base + (warp - 2) * kWarpStaging);
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa(smem_u32(&tempty[1]), 0);
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t use = 0;  // accumulator uses (same sequence as the MMA issuer)
     int slot = 0;
     uint32_t tq_phase = 0;
     while (true) {
@@ -492,14 +572,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         tq_phase ^= 1;
       }
       if (t >= total) break;
-      const TileCoord c = tile_coord(p, t, total);
-      mbar_wait(&tfull[acc], acc_phase);
+      const TileCoord c = tile_coord(p, t);
+      for (int sub = 0; sub < (c.half_hi ? 2 : 1); ++sub, ++use) {
+      const int acc = use & 1;
+      mbar_wait(&tfull[acc], (use >> 1) & 1);
       tc_fence_after();
       const uint32_t d = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
-      // accumulator column j <-> token row r0 + j (CTA 0 loaded rows [0, half),
-      // CTA 1 rows [half, 2*half) of the tile)
-      for (int c0 = grp * kEpiCols; c0 < ((p.dbg & 1) ? 0 : c.rows); c0 += kEpiGroups * kEpiCols) {
-        const int rows = min(kEpiCols, c.rows - c0);
+      // accumulator column j <-> token row sr0 + j (CTA 0 loaded rows [0, half),
+      // CTA 1 rows [half, 2*half) of the sub-tile)
+      const int sr0 = c.r0 + sub * p.tile_n;
+      const int srows = sub ? c.rows - p.tile_n : min(c.rows, p.tile_n);
+      for (int c0 = grp * kEpiCols; c0 < ((p.dbg & 1) ? 0 : srows); c0 += kEpiGroups * kEpiCols) {
+        const int rows = min(kEpiCols, srows - c0);
         if (MODE == kSwiglu) {
           // TMEM lanes 16b..16b+7 hold the gate rows and 16b+8..16b+15 the up
           // rows of CTA-local features 8b..8b+7 (the 4-D weight map's
@@ -522,7 +606,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               }
           }
           __syncwarp();
-          __nv_bfloat16 *obase = p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 128 +
+          __nv_bfloat16 *obase = p.out + (size_t)(sr0 + c0) * p.out_ld + c.m * 128 +
                                  (int)crank * 64 + quad * 16;
           for (int i = lane; i < rows * 2; i += 32) {  // 16 features = 2 x 16 B per row
             const int rr = i >> 1, ch = i & 1;
@@ -536,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) stg[j * 32 + lane] = __float2bfloat16_rn(v[j]);
           __syncwarp();
-          __nv_bfloat16 *obase = p.out + (size_t)(c.r0 + c0) * p.out_ld + c.m * 256 +
+          __nv_bfloat16 *obase = p.out + (size_t)(sr0 + c0) * p.out_ld + c.m * 256 +
                                  (int)crank * 128 + quad * 32;
           for (int i = lane; i < rows * 4; i += 32) {  // 32 features = 4 x 16 B per row
             const int rr = i >> 2, ch = i & 3;
@@ -552,9 +636,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // above) must precede the MMA's reuse of the accumulator; a release
       // arrive would also wait for this warp's global stores to be acked
       if (lane == 0) mbar_arrive_cluster_relaxed(acc ? tempty_leader1 : tempty_leader0);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
       }
     }
   }
@@ -673,11 +754,6 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   g.group_off = group_off;
   g.tile_off = tile_off;
   g.tile_n = p.tile_n;
-  static const int order = [] {
-    const char *e = getenv("JANUS_TILE_ORDER");
-    return e ? atoi(e) : 1;
-  }();
-  g.order = order;
   static const int dbg = [] {
     const char *e = getenv("JANUS_GEMM_DBG");
     return e ? atoi(e) : 0;

@@ -32,6 +32,7 @@ struct SchedArgs {
   int tile_n;          // token rows per GEMM n-tile (64 or 256)
   uint64_t *trace;     // [7] phase timestamps (%globaltimer), optional
   int id_bits;         // bits of the largest expert id (ballot-based peer matching)
+  int merge_tail;      // 1: a group's last n-tile also takes the remainder (wide tiles)
 };
 
 inline int id_bits_for(int E) {

@@ -67,6 +67,9 @@ def main():
         if name == "dense8":
             rmap = J.ReplicaMap.from_hosts(1, 8, [[0]] * 8)
             ex = np.tile(np.arange(8, dtype=np.int32), T)
+        elif name == "bal128":  # every expert exactly T*8/128 rows
+            rmap = J.ReplicaMap.from_hosts(1, 128, [[0]] * 128)
+            ex = ((np.arange(T)[:, None] * 8 + np.arange(8)[None, :]) % 128).astype(np.int32).ravel()
         elif name == "uni128":
             rmap = J.ReplicaMap.from_hosts(1, 128, [[0]] * 128)
             ex = J.gen_batch(J.RoutingPattern.uniform(128), T, K, 0x77, 0).experts
