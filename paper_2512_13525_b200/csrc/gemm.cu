@@ -66,6 +66,7 @@ enum Mode { kSwiglu = 0, kPlain = 1 };
 struct GemmParams {
   CUtensorMap tm_a;     // weights; SWIGLU: 4-D gate/up interleave map (box = 128 rows), PLAIN: 2-D, box 128 rows
   CUtensorMap tm_b[5];  // activations [S_alloc][K], box rows 8/16/32/64/128 (= N/2)
+  CUtensorMap tm_out;   // output [S_alloc][out_ld], no swizzle, box {kF features, 32 rows}
   const int32_t *group_off;
   const int32_t *tile_off;  // n-tiles of tile_n rows per group (prefix)
   unsigned *ctr;            // [2] next-tile counter, finished CTAs (reset by the last CTA)
@@ -246,6 +247,26 @@ __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+// Four 8x8 b16 matrices from mma-fragment registers, stored transposed: lane l
+// supplies the smem address of row l%8 of matrix l/8.
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t addr, uint32_t a0, uint32_t a1,
+                                                  uint32_t a2, uint32_t a3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+               "r"(a0), "r"(a1), "r"(a2), "r"(a3)
+               : "memory");
+}
+// TMA store of one box from smem (bulk async-group of the issuing thread).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
 }
 
 struct TileCoord {
@@ -584,48 +605,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int srows = sub ? c.rows - p.tile_n : min(c.rows, p.tile_n);
       for (int c0 = grp * kEpiCols; c0 < ((p.dbg & 1) ? 0 : srows); c0 += kEpiGroups * kEpiCols) {
         const int rows = min(kEpiCols, srows - c0);
-        if (MODE == kSwiglu) {
-          // TMEM lanes 16b..16b+7 hold the gate rows and 16b+8..16b+15 the up
-          // rows of CTA-local features 8b..8b+7 (the 4-D weight map's
-          // interleave).  The 16x256b shape gives each thread gate and up of
-          // one feature for two adjacent columns per 8-column repeat, so
-          // silu(g)*u is formed in registers.  This warp: features 16*quad..+15.
-          const int fq = lane >> 2, cq = 2 * (lane & 3);
+        // Output block of this warp: 32 token rows x kF features (SWIGLU: 16
+        // features of h, PLAIN: 32 of y).  The 16x256b TMEM shape hands each
+        // thread the mma-fragment layout (feature lane/4 and lane/4+8, token
+        // pair 2*(lane%4)), which stmatrix.trans writes into the staging tile
+        // as [token][feature] rows; one TMA store then moves the block.
+        constexpr int kF = MODE == kSwiglu ? 16 : 32;
+        const int f_base = MODE == kSwiglu ? c.m * 128 + (int)crank * 64 + quad * 16
+                                           : c.m * 256 + (int)crank * 128 + quad * 32;
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free again
+        __syncwarp();
+        const uint32_t stg_a = smem_u32(stg);
 #pragma unroll
-          for (int bb = 0; bb < 2; ++bb) {
-            uint32_t r[16];
-            tmem_ld_16x256b_x4(d + ((uint32_t)(16 * bb) << 16) + c0, r);
-            const int f = 8 * bb + fq;
+        for (int h = 0; h < 2; ++h) {  // TMEM lanes 16h..16h+15 of this warp's quarter
+          uint32_t r[16];
+          tmem_ld_16x256b_x4(d + ((uint32_t)(16 * h) << 16) + c0, r);
+          uint32_t pk[8];  // pk[2i + j]: feature block j of this 16-lane group, tokens 8i..8i+7
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i) {
+            if (MODE == kSwiglu) {
+              // lanes 16h..+7 gate, 16h+8..+15 up of features 8h..8h+7
+              float hv[2];
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const float g = __uint_as_float(r[4 * i + e]), u = __uint_as_float(r[4 * i + 2 + e]);
-                stg[(8 * i + cq + e) * 16 + f] =
-                    __float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u);
+                hv[e] = __fdividef(g, 1.0f + __expf(-g)) * u;
               }
+              pk[2 * i] = pack_bf16(hv[0], hv[1]);
+            } else {
+              pk[2 * i] = pack_bf16(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]));
+              pk[2 * i + 1] = pack_bf16(__uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+            }
           }
-          __syncwarp();
-          __nv_bfloat16 *obase = p.out + (size_t)(sr0 + c0) * p.out_ld + c.m * 128 +
-                                 (int)crank * 64 + quad * 16;
-          for (int i = lane; i < rows * 2; i += 32) {  // 16 features = 2 x 16 B per row
-            const int rr = i >> 1, ch = i & 1;
-            *reinterpret_cast<uint4 *>(obase + (size_t)rr * p.out_ld + ch * 8) =
-                *reinterpret_cast<const uint4 *>(stg + rr * 16 + ch * 8);
-          }
-          __syncwarp();
-        } else {
-          float v[32];
-          tmem_ld32(d + c0, v);
+          // 8x8 matrices (feature block fb, token block i) -> staging rows 8i..8i+7
+          const int q8 = lane >> 3, rr = lane & 7;
+          if (MODE == kSwiglu) {
+            // features 8h..8h+7 of this warp's 16: one x4 per (h), token blocks 0..3
+            stmatrix_x4_trans(stg_a + ((8 * q8 + rr) * kF + 8 * h) * 2, pk[0], pk[2], pk[4], pk[6]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) stg[j * 32 + lane] = __float2bfloat16_rn(v[j]);
+            for (int x = 0; x < 2; ++x) {  // token blocks 2x, 2x+1; feature blocks 2h, 2h+1
+              const int fb = 2 * h + (q8 & 1), i = 2 * x + (q8 >> 1);
+              stmatrix_x4_trans(stg_a + ((8 * i + rr) * kF + 8 * fb) * 2, pk[4 * x], pk[4 * x + 1],
+                                pk[4 * x + 2], pk[4 * x + 3]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging -> TMA (async proxy)
+        __syncwarp();
+        if (rows == kEpiCols) {
+          if (elect_one()) {
+            tma_store_2d(&p.tm_out, stg_a, f_base, sr0 + c0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
           __syncwarp();
-          __nv_bfloat16 *obase = p.out + (size_t)(sr0 + c0) * p.out_ld + c.m * 256 +
-                                 (int)crank * 128 + quad * 32;
-          for (int i = lane; i < rows * 4; i += 32) {  // 32 features = 4 x 16 B per row
-            const int rr = i >> 2, ch = i & 3;
-            *reinterpret_cast<uint4 *>(obase + (size_t)rr * p.out_ld + ch * 8) =
-                *reinterpret_cast<const uint4 *>(stg + rr * 32 + ch * 8);
+        } else {  // ragged tail of the sub-tile: 16-B stores
+          __nv_bfloat16 *obase = p.out + (size_t)(sr0 + c0) * p.out_ld + f_base;
+          constexpr int kV = kF / 8;  // 16-B pieces per row
+          for (int i = lane; i < rows * kV; i += 32) {
+            const int rw = i / kV, ch = i % kV;
+            *reinterpret_cast<uint4 *>(obase + (size_t)rw * p.out_ld + ch * 8) =
+                *reinterpret_cast<const uint4 *>(stg + rw * kF + ch * 8);
           }
           __syncwarp();
         }
@@ -639,6 +679,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
     }
   }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // epilogue TMA stores done
   tc_fence_before();
   cluster_sync_all();
   if (threadIdx.x == 0) {  // the last CTA to finish resets the tile counter for the next launch
@@ -697,6 +738,20 @@ bool make_map(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t cols, u
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Epilogue output map: bf16 [rows][cols], no swizzle, box {box_cols, 32 rows}.
+bool make_out_map(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t cols,
+                  uint32_t box_cols) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // The gate/up weight store [Q][gate d_e | up d_e][d_h] as a 4-D map {k, row in
 // an 8-row block, gate/up (+d_e rows), 8-row block}: one box {64, 8, 2, 8}
 // lands as 8 x (8 gate rows, the 8 up rows of the same features) — the row
@@ -722,6 +777,10 @@ cudaError_t build_ffn_tensor_maps(FfnPlan &p) {
   for (int i = 0; i < 5 && ok; ++i) {
     ok = make_map(&p.tm_xp[i], p.xp, p.S_alloc, p.d_h, 8u << i) &&
          make_map(&p.tm_h[i], p.h, p.S_alloc, p.d_e, 8u << i);
+  }
+  if (ok) {
+    ok = make_out_map(&p.tm_h_out, p.h, p.S_alloc, p.d_e, 16) &&
+         make_out_map(&p.tm_y_out, p.y, p.S_alloc, p.d_h, 32);
   }
   p.maps_ready = ok;
   return ok ? cudaSuccess : cudaErrorInvalidValue;
@@ -767,6 +826,7 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   // gate + up -> h: per replica A rows [gate d_e | up d_e]; 128 features per tile
   g.tm_a = p.tm_w13;
   for (int i = 0; i < 5; ++i) g.tm_b[i] = p.tm_xp[i];
+  g.tm_out = p.tm_h_out;
   g.K = p.d_h;
   g.m_tiles = p.d_e / 128;
   g.m_per_q = 2 * p.d_e;
@@ -779,6 +839,7 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   // down: y = h Wd^T, 256 output features per tile
   g.tm_a = p.tm_w2;
   for (int i = 0; i < 5; ++i) g.tm_b[i] = p.tm_h[i];
+  g.tm_out = p.tm_y_out;
   g.ctr = p.tile_ctr + 2;
   g.K = p.d_e;
   g.m_tiles = p.d_h / 256;

@@ -57,6 +57,7 @@ struct FfnPlan {
   unsigned *tile_ctr = nullptr;  // [4] per GEMM: next-tile counter, finished CTAs (self-resetting)
   CUtensorMap tm_w13, tm_w2;
   CUtensorMap tm_xp[5], tm_h[5];  // box rows 8/16/32/64/128 (half of a pair's N)
+  CUtensorMap tm_h_out, tm_y_out;  // epilogue TMA stores (box 16 / 32 features x 32 rows)
   bool maps_ready = false;
 };
 
