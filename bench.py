@@ -399,7 +399,8 @@ def run_box(args):
         rmap = J.config_map(MAP if M == 1 else f"{MAP}_m{M}")
         layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
-    box = JanusBox(plan, rank, T, D_H, K_TOP, layer=layer, device=local)
+    box = JanusBox(plan, rank, T, D_H, K_TOP, layer=layer, device=local,
+                   transport=args.transport)
     pat = J.RoutingPattern.zipf(E, 1.0)
     batches = [torch.from_numpy(J.gen_batch(pat, T, K_TOP, SEED, T * 1000 + i).experts).to(dev)
                for i in range(N_BATCHES)]
@@ -413,18 +414,24 @@ def run_box(args):
     stream = s.cuda_stream
     epoch = [0]
 
-    def step(i, xin=None, exin=None, gwin=None, o=None):
-        epoch[0] += 1
+    # Two steps in flight (the exchange double-buffers by epoch parity): an
+    # attention rank dispatches step i+1 before it combines step i, so the MoE
+    # GPUs find step i+1's rows already delivered when they finish step i.
+    def run_steps(n, i0=0):
+        e0_ = epoch[0]
         if role == "attention":
-            box.dispatch(xin if xin is not None else xs, exin if exin is not None else
-                         exs[i % N_BATCHES], gwin if gwin is not None else gws[0], T, epoch[0],
-                         stream)
-            box.combine(o if o is not None else out, T, epoch[0], stream)
+            box.dispatch(xs, exs[i0 % N_BATCHES], gws[0], T, e0_ + 1, stream)
+            for j in range(n):
+                if j + 1 < n:
+                    box.dispatch(xs, exs[(i0 + j + 1) % N_BATCHES], gws[0], T, e0_ + j + 2,
+                                 stream)
+                box.combine(out, T, e0_ + j + 1, stream)
         else:
-            box.moe_step(T, epoch[0], stream)
+            for j in range(n):
+                box.moe_step(T, e0_ + j + 1, stream)
+        epoch[0] += n
 
-    for i in range(args.warmup):
-        step(i)
+    run_steps(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
     if layer is not None:
@@ -433,8 +440,7 @@ def run_box(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(s)
-        for i in range(args.steps):
-            step(i)
+        run_steps(args.steps)
         e1.record(s)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -447,30 +453,48 @@ def run_box(args):
         ffn = [a_.value / max(c_.value, 1), b_.value / max(c_.value, 1), 1.0]
     # dispatch kernel alone (attention ranks): events around the dispatch only,
     # over extra steps after the timed region
-    disp_ms = 0.0
+    # each phase alone, one step in flight: attention dispatch; MoE step (from
+    # its inputs being present); attention combine (after every MoE published)
+    disp_ms = moe_ms = comb_ms = 0.0
     dist.barrier()
     nd = 20
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     for i in range(nd):
         epoch[0] += 1
         if role == "attention":
-            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0, d1 = ev(), ev()
             d0.record(s)
             box.dispatch(xs, exs[i % N_BATCHES], gws[0], T, epoch[0], stream)
             d1.record(s)
-            box.combine(out, T, epoch[0], stream)
             torch.cuda.synchronize()
             disp_ms += d0.elapsed_time(d1) / nd
-        else:
+        dist.barrier()
+        if role == "moe":
+            m0, m1 = ev(), ev()
+            m0.record(s)
             box.moe_step(T, epoch[0], stream)
+            m1.record(s)
+            torch.cuda.synchronize()
+            moe_ms += m0.elapsed_time(m1) / nd
+        dist.barrier()
+        if role == "attention":
+            c0, c1 = ev(), ev()
+            c0.record(s)
+            box.combine(out, T, epoch[0], stream)
+            c1.record(s)
+            torch.cuda.synchronize()
+            comb_ms += c0.elapsed_time(c1) / nd
     torch.cuda.synchronize()
     dist.barrier()
-    tvec = torch.tensor([ms, ffn[1], float(launches), disp_ms], device=dev)
+    tvec = torch.tensor([ms, ffn[1], float(launches), disp_ms, moe_ms, comb_ms], device=dev)
     allv = [torch.zeros_like(tvec) for _ in range(ws)]
     dist.all_gather(allv, tvec)
     ms_max = max(float(v[0]) for v in allv)
     ffn_ms = max(float(v[1]) for v in allv)  # slowest MoE GPU's grouped GEMMs
     launches_all = int(sum(float(v[2]) for v in allv))
     disp_ms = max(float(v[3]) for v in allv)
+    moe_ms = max(float(v[4]) for v in allv)
+    comb_ms = max(float(v[5]) for v in allv)
 
     # e2e through the host API: attention ranks copy their shard in from pinned
     # host memory and their outputs back each step
@@ -482,16 +506,31 @@ def run_box(args):
         xd, exd, gwd = torch.empty_like(xs), torch.empty_like(exs[0]), torch.empty_like(gws[0])
     dist.barrier()
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        if role == "attention":
-            xd.copy_(xh, non_blocking=True)
-            exd.copy_(exh[i % N_BATCHES], non_blocking=True)
-            gwd.copy_(gwh, non_blocking=True)
-            step(i, xd, exd, gwd, out)
+    e0_ = epoch[0]
+    if role == "attention":
+        # per step: H2D of step i+1's shard, dispatch i+1, combine i, D2H of i
+        xd2 = [xd, torch.empty_like(xd)]
+        exd2 = [exd, torch.empty_like(exd)]
+        gwd2 = [gwd, torch.empty_like(gwd)]
+
+        def h2d_dispatch(i):
+            b = i & 1
+            xd2[b].copy_(xh, non_blocking=True)
+            exd2[b].copy_(exh[i % N_BATCHES], non_blocking=True)
+            gwd2[b].copy_(gwh, non_blocking=True)
+            box.dispatch(xd2[b], exd2[b], gwd2[b], T, e0_ + i + 1, stream)
+
+        h2d_dispatch(0)
+        for i in range(args.steps):
+            if i + 1 < args.steps:
+                h2d_dispatch(i + 1)
+            box.combine(out, T, e0_ + i + 1, stream)
             oh.copy_(out, non_blocking=True)
             torch.cuda.synchronize()
-        else:
-            step(i)
+    else:
+        for i in range(args.steps):
+            box.moe_step(T, e0_ + i + 1, stream)
+    epoch[0] += args.steps
     torch.cuda.synchronize()
     dist.barrier()
     e2e_s = time.perf_counter() - t0
@@ -513,7 +552,10 @@ def run_box(args):
             "config": {"workload": f"c2 expert shape (Qwen3-30B-A3B: 128 experts, top-8, "
                                    f"d_h 2048, d_e 768) on one NVLink box split {A} attention + "
                                    f"{M} MoE GPUs; attention->MoE dispatch and MoE->attention "
-                                   f"combine by peer-memory kernels",
+                                   f"combine by " + ("NVSwitch multicast (NVLS) kernels"
+                                                     if box.transport == "nvls"
+                                                     else "peer-memory (P2P) kernels"),
+                       "transport": box.transport,
                        "tokens_per_step": T, "tokens_per_moe_gpu": args.tokens,
                        "replica_map": f"maps/{MAP if M == 1 else f'{MAP}_m{M}'}.map",
                        "parallelism": f"{A}A+{M}E", "l2": "inputs > L2 (weights streamed)"},
@@ -522,11 +564,20 @@ def run_box(args):
                          "ffn_us_per_step": ffn_ms * 1e3, "achieved": None, "peak": hbm,
                          "unit": "GB/s", "frac": None, "traffic": None,
                          "peak_source": f"{src} (MEASURED_PEAKS.json)"},
-            "nvlink": {"dispatch_bytes_per_step_per_attention_gpu": send_bytes,
+            "nvlink": {"transport": box.transport,
+                       # P2P: the attention GPU stores each row once per MoE GPU;
+                       # NVLS: once, the switch fans it out to the M MoE GPUs
+                       "dispatch_egress_bytes_per_step_per_attention_gpu":
+                           send_bytes // (M if box.transport == "nvls" else 1),
+                       "dispatch_bytes_per_step_per_attention_gpu": send_bytes,
                        "combine_bytes_per_step_per_attention_gpu": sends[0][1],
                        "dispatch_us": disp_ms * 1e3,
+                       "moe_step_us": moe_ms * 1e3,
+                       "combine_us": comb_ms * 1e3,
                        "dispatch_achieved_gbs": send_bytes / (disp_ms / 1e3) / 1e9
                        if disp_ms > 0 else None,
+                       "dispatch_egress_gbs": send_bytes // (M if box.transport == "nvls" else 1)
+                       / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else None,
                        "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy "
                                                          "per direction (fallback)"},
             "e2e": {"value": T * args.steps / e2e_s, "unit": "tokens/s",
@@ -549,6 +600,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls"],
+                    help="box exchange for --gpus > 1 (auto: NVLS multicast when supported)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

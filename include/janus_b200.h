@@ -177,6 +177,18 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t num_t
                                       uint64_t epoch, void *stream);
 /* host: 1 if a wait exceeded its bound (a peer never published). */
 janus_status janus_xfer_status(janus_ctx *ctx, int *timed_out);
+/* NVLS multicast transport (optional, after janus_xfer_connect on every rank):
+ * rows, routing and partial sums then move through one NVSwitch multicast
+ * object — dispatch leaves an attention GPU once instead of once per MoE GPU,
+ * and the combine's sum over MoE GPUs is done by the switch
+ * (multimem.ld_reduce).  Rank 0 creates it and exports a POSIX fd, which the
+ * caller passes to every other rank (e.g. SCM_RIGHTS); each other rank joins
+ * with it; after all ranks joined, every rank binds its backing.  Flags keep
+ * using the IPC regions.  Without this call sequence the P2P path is used. */
+janus_status janus_xfer_mc_supported(janus_ctx *ctx, int *yes);
+janus_status janus_xfer_mc_create(janus_ctx *ctx, int *fd);
+janus_status janus_xfer_mc_join(janus_ctx *ctx, int fd);
+janus_status janus_xfer_mc_bind(janus_ctx *ctx);
 
 /* ---- model / workload --------------------------------------------------- */
 /* The reference roofline prediction (latency.cpp:17-32), kept for comparison

@@ -26,7 +26,8 @@ SYMBOLS = (
     "janus_moe_layer_latency", "janus_gen_batch", "janus_derive_seed", "janus_profile",
     "janus_profile_read", "janus_trace_schedule", "janus_xfer_configure", "janus_xfer_handle",
     "janus_xfer_connect", "janus_attn_dispatch_async", "janus_moe_layer_xfer_async",
-    "janus_attn_combine_async", "janus_xfer_status",
+    "janus_attn_combine_async", "janus_xfer_status", "janus_xfer_mc_supported",
+    "janus_xfer_mc_create", "janus_xfer_mc_join", "janus_xfer_mc_bind",
 )
 
 
@@ -76,6 +77,10 @@ def _load() -> C.CDLL:
     L.janus_moe_layer_xfer_async.argtypes = [vp, i64, u64, vp]
     L.janus_attn_combine_async.argtypes = [vp, vp, i64, u64, vp]
     L.janus_xfer_status.argtypes = [vp, P(i32)]
+    L.janus_xfer_mc_supported.argtypes = [vp, P(i32)]
+    L.janus_xfer_mc_create.argtypes = [vp, P(i32)]
+    L.janus_xfer_mc_join.argtypes = [vp, i32]
+    L.janus_xfer_mc_bind.argtypes = [vp]
     return L
 
 

@@ -42,7 +42,7 @@ namespace janus {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kMaxCluster = 8;
+constexpr int kMaxCluster = 16;  // non-portable above 8 (one GPC holds 16+ SMs on B200)
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t &s) {
   s += 0x9e3779b97f4a7c15ULL;
@@ -454,6 +454,9 @@ cudaError_t launch_variant(const SchedArgs &a, size_t smem, int csize, cudaStrea
     cudaError_t err = cudaFuncSetAttribute(aebs_schedule_kernel<MAXIT>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
     if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(aebs_schedule_kernel<MAXIT>,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return err;
     configured_dev = dev;
     configured_smem = want;
   }
@@ -480,7 +483,9 @@ size_t schedule_smem_bytes(int E, int N, int R) {
 }
 
 int schedule_cluster_size(int S) {
-  // aim at <= 2048 slots (2 windows per warp) per CTA, up to a portable cluster
+  // aim at <= 2048 slots (2 windows per warp) per CTA; above 8 CTAs (S > 16 K
+  // slots, e.g. the box path's MoE GPUs scheduling every attention shard) the
+  // cluster grows to 16
   int c = (S + 2047) / 2048;
   return c < 1 ? 1 : (c > kMaxCluster ? kMaxCluster : c);
 }

@@ -155,6 +155,7 @@ void janus_destroy(janus_ctx *ctx) {
   for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
   for (auto &g : ctx->graphs) cudaGraphExecDestroy(g.exec);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  janus::mc_free(ctx->xfer, ctx->device);
   for (void *p : ctx->xfer.opened) cudaIpcCloseMemHandle(p);
   dfree(ctx->xfer.local);
   dfree(ctx->xfer.counter);
@@ -527,7 +528,17 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
   e = janus::launch_ffn(p, a.group_off, ctx->ws_tile_off, s, &launches);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "grouped_gemm_kernel");
   if (ev) CK(cudaEventRecord(ev[3], s));
-  if (push_epoch)
+  if (push_epoch && ctx->xfer.mc) {
+    // multicast: partial sums of this instance for every token into the own
+    // backing (the attention ranks' switch-reduced reads add them up), flag
+    const janus::XferState &x = ctx->xfer;
+    e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
+                              reinterpret_cast<void *>(x.uc_va + x.mpart_off +
+                                                       janus::xfer_slot(push_epoch) * x.mslot),
+                              s);
+    if (e == cudaSuccess) e = janus::launch_signal_combine(x, push_epoch, s);
+    launches += 1;
+  } else if (push_epoch)
     e = janus::launch_combine_push(ctx->xfer, p.y, a.slot_row, a.instance, d_gate_w, T,
                                    push_epoch, s);
   else
@@ -602,6 +613,7 @@ janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int ran
     return fail(ctx, JANUS_EUNSUPPORTED, "xfer: at most 16 ranks in one box");
   CK(cudaSetDevice(ctx->device));
   janus::XferState &x = ctx->xfer;
+  janus::mc_free(x, ctx->device);
   if (x.local) cudaFree(x.local);
   for (void *p : x.opened) cudaIpcCloseMemHandle(p);
   dfree(x.counter);
@@ -679,7 +691,14 @@ janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoc
   cudaError_t e = janus::launch_wait(x, true, epoch, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
   ctx->launches += 1;
-  unsigned char *base = static_cast<unsigned char *>(x.local);
+  if (x.mc) {  // rows / routing landed in this rank's multicast backing
+    unsigned char *base = reinterpret_cast<unsigned char *>(x.uc_va) + janus::xfer_slot(epoch) * x.mslot;
+    return layer_run(ctx, base + x.mx_off, reinterpret_cast<const int32_t *>(base + x.mex_off),
+                     reinterpret_cast<const float *>(base + x.mgw_off), (int)T, nullptr, nullptr,
+                     s, epoch);
+  }
+  unsigned char *base =
+      static_cast<unsigned char *>(x.local) + janus::xfer_slot(epoch) * x.L.slot_stride;
   return layer_run(ctx, base + x.L.x_off, reinterpret_cast<const int32_t *>(base + x.L.ex_off),
                    reinterpret_cast<const float *>(base + x.L.gw_off), (int)T, nullptr, nullptr, s,
                    epoch);
@@ -694,9 +713,43 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, ui
   janus_shard_tokens(T, x.A, x.rank, &first, &Ta);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = janus::launch_wait(x, false, epoch, s);
-  if (e == cudaSuccess) e = janus::launch_reduce_partials(x, d_out, Ta, s);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "reduce_partials_kernel");
+  if (e == cudaSuccess)
+    e = x.mc ? janus::launch_reduce_mc(x, d_out, first, Ta, epoch, s)
+             : janus::launch_reduce_partials(x, d_out, Ta, epoch, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, x.mc ? "reduce_mc_kernel" : "reduce_partials_kernel");
   ctx->launches += 2;
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_mc_supported(janus_ctx *ctx, int *yes) {
+  if (!ctx || !yes) return JANUS_EINVAL;
+  *yes = janus::mc_supported(ctx->device) ? 1 : 0;
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_mc_create(janus_ctx *ctx, int *fd) {
+  if (!ctx || !fd) return JANUS_EINVAL;
+  if (!ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: connect before the multicast setup");
+  CK(cudaSetDevice(ctx->device));
+  const std::string e = janus::mc_create(ctx->xfer, ctx->device, fd);
+  if (!e.empty()) return fail(ctx, JANUS_ECUDA, e);
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_mc_join(janus_ctx *ctx, int fd) {
+  if (!ctx) return JANUS_EINVAL;
+  if (!ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: connect before the multicast setup");
+  CK(cudaSetDevice(ctx->device));
+  const std::string e = janus::mc_join(ctx->xfer, ctx->device, fd);
+  if (!e.empty()) return fail(ctx, JANUS_ECUDA, e);
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_mc_bind(janus_ctx *ctx) {
+  if (!ctx) return JANUS_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const std::string e = janus::mc_bind(ctx->xfer, ctx->device);
+  if (!e.empty()) return fail(ctx, JANUS_ECUDA, e);
   return JANUS_OK;
 }
 

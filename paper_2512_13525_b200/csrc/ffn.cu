@@ -42,11 +42,7 @@ __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__res
   const int t = task / segs, c0 = (task % segs) * 32 * kPermU + lane;
   const uint4 *src = x + (size_t)t * vec;
   uint4 v[kPermU];
-#pragma unroll
-  for (int u = 0; u < kPermU; ++u) {
-    const int c = c0 + 32 * u;
-    if (c < vec) v[u] = __ldg(src + c);
-  }
+  bool loaded = false;  // x is read only if some slot of t is routed here
   for (int j0 = 0; j0 < k; j0 += 32) {
     const int j = j0 + lane;
     int row = -1;
@@ -54,10 +50,17 @@ __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__res
       const int s = t * k + j;
       if (instance < 0 || __ldg(slot_inst + s) == instance) row = __ldg(slot_row + s);
     }
-    const int n = min(32, k - j0);
-    for (int jj = 0; jj < n; ++jj) {
-      const int r = __shfl_sync(0xffffffffu, row, jj);
-      if (r < 0) continue;
+    unsigned m = __ballot_sync(0xffffffffu, row >= 0);
+    if (m && !loaded) {
+#pragma unroll
+      for (int u = 0; u < kPermU; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < vec) v[u] = __ldg(src + c);
+      }
+      loaded = true;
+    }
+    for (; m; m &= m - 1) {
+      const int r = __shfl_sync(0xffffffffu, row, __ffs(m) - 1);
       uint4 *dst = xp + (size_t)r * vec;
 #pragma unroll
       for (int u = 0; u < kPermU; ++u) {
@@ -73,6 +76,11 @@ __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__res
 // (all slots when instance < 0), j ascending, fp32, then bf16.  One warp task
 // = one 32*U-chunk segment of token t; the row indices / weights are loaded by
 // lanes j < k and broadcast; 8 rows x U chunks are in flight per lane.
+// G = slots gathered per round (4: measured faster than 8 even with every
+// slot local — fewer registers, more warps; with the instance filter about k/M
+// of a token's slots are routed here and the ballot compaction keeps the loads
+// to the slots that exist).
+template <int G>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
     combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
                    const int32_t *__restrict__ slot_inst, int instance,
@@ -99,34 +107,38 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
       }
     }
     const int n = min(32, k - j0);
-    for (int jj = 0; jj < n; jj += 8) {
-      uint4 v[8][kCombU];
-      float wv[8];
-      const uint4 *src[8];
-      bool ok[8];
+    // lanes holding a slot routed here, taken in ascending j, G per round
+    unsigned m = __ballot_sync(0xffffffffu, lane < n && row >= 0);
+    while (m) {
+      uint4 v[G][kCombU];
+      float wv[G];
+      const uint4 *src[G];
+      bool ok[G];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int r = __shfl_sync(0xffffffffu, row, (jj + b) & 31);
-        const float wb = __shfl_sync(0xffffffffu, w, (jj + b) & 31);
-        ok[b] = jj + b < n && r >= 0;
+      for (int b = 0; b < G; ++b) {
+        ok[b] = m != 0;
+        const int ln = ok[b] ? __ffs(m) - 1 : 0;
+        m &= m - 1;
+        const int r = __shfl_sync(0xffffffffu, row, ln);
+        const float wb = __shfl_sync(0xffffffffu, w, ln);
         wv[b] = ok[b] ? wb : 0.f;
         src[b] = y + (size_t)(ok[b] ? r : 0) * vec;  // clamped; masked below
       }
-      // all 8 x U loads are issued before the first is consumed
+      // all G x U loads are issued before the first is consumed
 #pragma unroll
-      for (int b = 0; b < 8; ++b)
+      for (int b = 0; b < G; ++b)
 #pragma unroll
         for (int u = 0; u < kCombU; ++u) {
           const int c = c0 + 32 * u;
           v[b][u] = ld_nc(src[b] + min(c, vec - 1));
         }
 #pragma unroll
-      for (int b = 0; b < 8; ++b)
+      for (int b = 0; b < G; ++b)
 #pragma unroll
         for (int u = 0; u < kCombU; ++u)
           if (!ok[b] || c0 + 32 * u >= vec) v[b][u] = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int b = 0; b < 8; ++b)  // fixed j order: bitwise reproducible
+      for (int b = 0; b < G; ++b)  // fixed j order: bitwise reproducible
 #pragma unroll
         for (int u = 0; u < kCombU; ++u) {
           const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v[b][u]);
@@ -172,9 +184,9 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
   const int vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kCombU - 1) / (32 * kCombU));
   const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  combine_kernel<<<blocks, 32 * kWarpsPerBlock, 0, s>>>(reinterpret_cast<const uint4 *>(y),
-                                                        slot_row, slot_instance, instance, gate_w,
-                                                        T, k, vec, reinterpret_cast<uint4 *>(out));
+  combine_kernel<4><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(
+      reinterpret_cast<const uint4 *>(y), slot_row, slot_instance, instance, gate_w, T, k, vec,
+      reinterpret_cast<uint4 *>(out));
   return cudaGetLastError();
 }
 

@@ -75,7 +75,9 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
 // ranks [A, A+M) are MoE instances g = rank - A.  One exchange region per
 // rank, identical layout everywhere.
 struct XferLayout {
-  size_t flag_dispatch_off, flag_combine_off, x_off, ex_off, gw_off, part_off, bytes;
+  // x/ex/gw/part offsets are slot 0's; slot 1 (odd epochs) is + slot_stride, so
+  // two steps can be in flight (dispatch of step s+1 while step s computes)
+  size_t flag_dispatch_off, flag_combine_off, x_off, ex_off, gw_off, part_off, slot_stride, bytes;
   long long ta_max;  // largest attention shard
 };
 XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k);
@@ -89,7 +91,20 @@ struct XferState {
   std::vector<void *> opened;         // IPC mappings to close
   unsigned *counter = nullptr;        // last-block counter (device)
   int *err = nullptr;                 // wait timeout flag (device)
+  // NVLS multicast transport (mc.cpp): the bulk rows / routing / partial sums
+  // go through one multicast object; flags stay in the IPC regions above.
+  bool mc = false, mc_bound = false;
+  unsigned long long mc_handle = 0, mem_handle = 0;  // CUmemGenericAllocationHandle
+  unsigned long long mc_va = 0, uc_va = 0;           // multicast / own-backing mappings
+  size_t mc_bytes = 0, mc_gran = 0;
+  size_t mx_off = 0, mex_off = 0, mgw_off = 0, mpart_off = 0, mslot = 0;  // slot 0; slot 1 = + mslot
 };
+
+bool mc_supported(int device);
+std::string mc_create(XferState &x, int device, int *fd);  // rank 0
+std::string mc_join(XferState &x, int device, int fd);     // other ranks
+std::string mc_bind(XferState &x, int device);             // every rank, after all joined
+void mc_free(XferState &x, int device);
 
 cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *d_ex,
                             const float *d_gw, long long T, unsigned long long epoch,
@@ -99,7 +114,14 @@ cudaError_t launch_wait(const XferState &x, bool dispatch_flags, unsigned long l
 cudaError_t launch_combine_push(const XferState &x, const void *y, const int32_t *slot_row,
                                 const int32_t *slot_inst, const float *gw, long long T,
                                 unsigned long long epoch, cudaStream_t s);
-cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta, cudaStream_t s);
+cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta,
+                                   unsigned long long epoch, cudaStream_t s);
+inline size_t xfer_slot(unsigned long long epoch) { return (size_t)(epoch & 1); }
+// multicast path: partial sums already in this MoE rank's backing -> raise the
+// attention ranks' combine flags; attention: switch-reduced read of its rows
+cudaError_t launch_signal_combine(const XferState &x, unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_reduce_mc(const XferState &x, void *d_out, long long first, long long Ta,
+                             unsigned long long epoch, cudaStream_t s);
 
 }  // namespace janus
 

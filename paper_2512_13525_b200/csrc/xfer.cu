@@ -87,10 +87,19 @@ __device__ __forceinline__ bool last_block(unsigned *counter) {
 // Attention rank `a`: push this shard's rows, routing and gate weights into
 // every MoE rank's receive buffers at the shard's token offset, then raise
 // flag_dispatch[a] = epoch on each MoE rank.
-__global__ void dispatch_kernel(PeerPtrs peers, int M, int A, int a, const uint4 *__restrict__ x,
-                                const int32_t *__restrict__ ex, const float *__restrict__ gw,
-                                long long first, long long Ta, int vec, int k, XferLayout L,
-                                unsigned long long epoch, unsigned *counter) {
+// Destinations: the M MoE ranks' IPC regions (P2P), or the one multicast
+// mapping (NVLS: the switch replicates each store to every rank).
+struct DispatchDst {
+  unsigned char *base[kMaxPeers];
+  int n;
+  size_t x_off, ex_off, gw_off;
+};
+
+__global__ void dispatch_kernel(DispatchDst dst, PeerPtrs peers, int M, int A, int a,
+                                const uint4 *__restrict__ x, const int32_t *__restrict__ ex,
+                                const float *__restrict__ gw, long long first, long long Ta,
+                                int vec, int k, XferLayout L, unsigned long long epoch,
+                                unsigned *counter) {
   const long long nx = Ta * vec, ns = Ta * k;
   const long long stride = (long long)gridDim.x * blockDim.x;
   // 4 independent 16-B chunks per thread per round: 4 loads in flight, then
@@ -104,21 +113,21 @@ __global__ void dispatch_kernel(PeerPtrs peers, int M, int A, int a, const uint4
       const long long i = i0 + u * stride;
       if (i < nx) v[u] = __ldg(x + i);
     }
-    for (int g = 0; g < M; ++g) {
-      uint4 *dst = reinterpret_cast<uint4 *>(peers.base[A + g] + L.x_off) + first * vec;
+    for (int g = 0; g < dst.n; ++g) {
+      uint4 *d = reinterpret_cast<uint4 *>(dst.base[g] + dst.x_off) + first * vec;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long i = i0 + u * stride;
-        if (i < nx) dst[i] = v[u];
+        if (i < nx) d[i] = v[u];
       }
     }
   }
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ns; i += stride) {
     const int32_t e = __ldg(ex + i);
     const float w = __ldg(gw + i);
-    for (int g = 0; g < M; ++g) {
-      reinterpret_cast<int32_t *>(peers.base[A + g] + L.ex_off)[first * k + i] = e;
-      reinterpret_cast<float *>(peers.base[A + g] + L.gw_off)[first * k + i] = w;
+    for (int g = 0; g < dst.n; ++g) {
+      reinterpret_cast<int32_t *>(dst.base[g] + dst.ex_off)[first * k + i] = e;
+      reinterpret_cast<float *>(dst.base[g] + dst.gw_off)[first * k + i] = w;
     }
   }
   if (last_block(counter) && threadIdx.x < M) {
@@ -156,8 +165,8 @@ __global__ void combine_push_kernel(PeerPtrs peers, int A, int g, const __nv_bfl
                                     const int32_t *__restrict__ slot_row,
                                     const int32_t *__restrict__ slot_inst,
                                     const float *__restrict__ gw, long long T, int k, int d_h,
-                                    long long ta_max, XferLayout L, unsigned long long epoch,
-                                    unsigned *counter) {
+                                    long long ta_max, XferLayout L, size_t part_off,
+                                    unsigned long long epoch, unsigned *counter) {
   const int vec = d_h / 8;
   const long long n = T * vec;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -188,7 +197,7 @@ __global__ void combine_push_kernel(PeerPtrs peers, int A, int g, const __nv_bfl
     int a;
     long long first;
     shard_of(T, A, t, a, first);
-    uint4 *dst = reinterpret_cast<uint4 *>(peers.base[a] + L.part_off) +
+    uint4 *dst = reinterpret_cast<uint4 *>(peers.base[a] + part_off) +
                  ((long long)g * ta_max + (t - first)) * vec;
     dst[c] = o;
   }
@@ -228,6 +237,48 @@ __global__ void reduce_partials_kernel(const __nv_bfloat16 *__restrict__ part, i
   }
 }
 
+// MoE rank g (multicast path): its partial sums are already in its own backing
+// (K5 with the instance filter); publish flag_combine[g] = epoch on every
+// attention rank.  The release store is cumulative over the preceding kernel's
+// writes (stream order), so the switch-side reads see them.
+__global__ void signal_combine_kernel(PeerPtrs peers, int A, int g, XferLayout L,
+                                      unsigned long long epoch) {
+  __threadfence_system();
+  if (threadIdx.x < A) {
+    unsigned long long *flag =
+        reinterpret_cast<unsigned long long *>(peers.base[threadIdx.x] + L.flag_combine_off) + g;
+    st_release_sys(flag, epoch);
+  }
+}
+
+// Attention rank (multicast path): out[t] = sum over every rank's backing of
+// part[first + t], reduced by the NVSwitch (multimem.ld_reduce, fp32
+// accumulation, one rounding to bf16).  Ranks that hold no partial for a row
+// contribute zeros.
+__global__ void reduce_mc_kernel(const uint4 *__restrict__ mc_part, long long n,
+                                 uint4 *__restrict__ out) {
+  constexpr int U = 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n)
+        asm volatile(
+            "multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+            : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+            : "l"(mc_part + i)
+            : "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n) out[i] = v[u];
+    }
+  }
+}
+
 int grid_for(long long work, int per_block = 256) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -254,6 +305,7 @@ XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
   o = up(o + 8 * (size_t)A);
   L.flag_combine_off = o;
   o = up(o + 8 * (size_t)M);
+  const size_t slot0 = o;
   L.x_off = o;
   o = up(o + (size_t)T_max * d_h * 2);
   L.ex_off = o;
@@ -262,7 +314,8 @@ XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
   o = up(o + (size_t)T_max * k * 4);
   L.part_off = o;
   o = up(o + (size_t)M * ta_max * d_h * 2);
-  L.bytes = o;
+  L.slot_stride = o - slot0;
+  L.bytes = o + L.slot_stride;
   L.ta_max = ta_max;
   return L;
 }
@@ -278,9 +331,25 @@ cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *
     first = a * base + std::min<long long>(a, rem);
   }
   const int vec = x.d_h / 8;
+  DispatchDst dst{};
+  if (x.mc) {  // one store per element; the NVSwitch replicates it to every rank
+    const size_t so = xfer_slot(epoch) * x.mslot;
+    dst.base[0] = reinterpret_cast<unsigned char *>(x.mc_va);
+    dst.n = 1;
+    dst.x_off = x.mx_off + so;
+    dst.ex_off = x.mex_off + so;
+    dst.gw_off = x.mgw_off + so;
+  } else {
+    const size_t so = xfer_slot(epoch) * x.L.slot_stride;
+    for (int g = 0; g < x.M; ++g) dst.base[g] = static_cast<unsigned char *>(x.peer_base[x.A + g]);
+    dst.n = x.M;
+    dst.x_off = x.L.x_off + so;
+    dst.ex_off = x.L.ex_off + so;
+    dst.gw_off = x.L.gw_off + so;
+  }
   dispatch_kernel<<<grid_for(std::max<long long>(Ta * vec, 1)), 256, 0, s>>>(
-      peer_ptrs(x), x.M, x.A, a, reinterpret_cast<const uint4 *>(d_x), d_ex, d_gw, first, Ta, vec,
-      x.k, x.L, epoch, x.counter);
+      dst, peer_ptrs(x), x.M, x.A, a, reinterpret_cast<const uint4 *>(d_x), d_ex, d_gw, first, Ta,
+      vec, x.k, x.L, epoch, x.counter);
   return cudaGetLastError();
 }
 
@@ -299,16 +368,36 @@ cudaError_t launch_combine_push(const XferState &x, const void *y, const int32_t
   const int g = x.rank - x.A;
   combine_push_kernel<<<grid_for(std::max<long long>(T * (x.d_h / 8), 1)), 256, 0, s>>>(
       peer_ptrs(x), x.A, g, reinterpret_cast<const __nv_bfloat16 *>(y), slot_row, slot_inst, gw,
-      T, x.k, x.d_h, x.L.ta_max, x.L, epoch, x.counter);
+      T, x.k, x.d_h, x.L.ta_max, x.L, x.L.part_off + xfer_slot(epoch) * x.L.slot_stride, epoch,
+      x.counter);
   return cudaGetLastError();
 }
 
-cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta, cudaStream_t s) {
+cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta,
+                                   unsigned long long epoch, cudaStream_t s) {
   if (Ta == 0) return cudaSuccess;
   const unsigned char *base = static_cast<const unsigned char *>(x.local);
   reduce_partials_kernel<<<grid_for(Ta * (x.d_h / 8)), 256, 0, s>>>(
-      reinterpret_cast<const __nv_bfloat16 *>(base + x.L.part_off), x.M, Ta, x.L.ta_max, x.d_h,
+      reinterpret_cast<const __nv_bfloat16 *>(base + x.L.part_off +
+                                               xfer_slot(epoch) * x.L.slot_stride),
+      x.M, Ta, x.L.ta_max, x.d_h,
       reinterpret_cast<__nv_bfloat16 *>(d_out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_signal_combine(const XferState &x, unsigned long long epoch, cudaStream_t s) {
+  signal_combine_kernel<<<1, 32, 0, s>>>(peer_ptrs(x), x.A, x.rank - x.A, x.L, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_mc(const XferState &x, void *d_out, long long first, long long Ta,
+                             unsigned long long epoch, cudaStream_t s) {
+  if (Ta == 0) return cudaSuccess;
+  const long long vec = x.d_h / 8, n = Ta * vec;
+  const uint4 *part =
+      reinterpret_cast<const uint4 *>(x.mc_va + x.mpart_off + xfer_slot(epoch) * x.mslot) +
+      first * vec;
+  reduce_mc_kernel<<<grid_for((n + 3) / 4), 256, 0, s>>>(part, n, reinterpret_cast<uint4 *>(d_out));
   return cudaGetLastError();
 }
 

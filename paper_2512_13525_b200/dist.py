@@ -93,7 +93,7 @@ class JanusBox:
     built with ``instance = rank - n_attn`` and its weight store set)."""
 
     def __init__(self, plan: BoxPlan, rank: int, max_tokens: int, d_hidden: int, top_k: int,
-                 layer=None, device: int = 0, group=None):
+                 layer=None, device: int = 0, group=None, transport: str = "auto"):
         import torch.distributed as dist
         self.plan, self.rank = plan, rank
         self.max_tokens, self.d_h, self.k = max_tokens, d_hidden, top_k
@@ -115,6 +115,55 @@ class JanusBox:
         handles = [None] * plan.world
         dist.all_gather_object(handles, bytes(h.raw), group=group)
         self._check(lib.janus_xfer_connect(self._ctx, b"".join(handles)))
+        dist.barrier(group=group)
+        self.transport = "p2p"
+        if transport not in ("auto", "p2p", "nvls"):
+            raise ValueError(transport)
+        if transport != "p2p":
+            yes = C.c_int()
+            self._check(lib.janus_xfer_mc_supported(self._ctx, C.byref(yes)))
+            every = [None] * plan.world
+            dist.all_gather_object(every, bool(yes.value), group=group)
+            if all(every):
+                self._setup_multicast(dist, group)
+                self.transport = "nvls"
+            elif transport == "nvls":
+                raise JanusError(5, "xfer: NVLS multicast not supported on every rank")
+
+    def _setup_multicast(self, dist, group) -> None:
+        """Rank 0 creates the multicast object; its POSIX fd reaches the other
+        ranks over a Unix socket (SCM_RIGHTS); all join, then all bind."""
+        import os
+        import socket
+        import tempfile
+        if self.rank == 0:
+            fd = C.c_int(-1)
+            self._check(lib.janus_xfer_mc_create(self._ctx, C.byref(fd)))
+            path = os.path.join(tempfile.gettempdir(), f"janus_mc_{os.getpid()}.sock")
+            if os.path.exists(path):
+                os.unlink(path)
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(path)
+            srv.listen(self.plan.world)
+            dist.broadcast_object_list([path], src=0, group=group)
+            for _ in range(self.plan.world - 1):
+                conn, _ = srv.accept()
+                socket.send_fds(conn, [b"fd"], [fd.value])
+                conn.close()
+            srv.close()
+            os.unlink(path)
+            os.close(fd.value)
+        else:
+            obj = [None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            cli.connect(obj[0])
+            _, fds, _, _ = socket.recv_fds(cli, 16, 1)
+            cli.close()
+            self._check(lib.janus_xfer_mc_join(self._ctx, fds[0]))
+            os.close(fds[0])
+        dist.barrier(group=group)
+        self._check(lib.janus_xfer_mc_bind(self._ctx))
         dist.barrier(group=group)
 
     def _check(self, st):

@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--tokens", type=int, default=300)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls"])
+    ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
+                    help="2: dispatch step s+1 before combining step s (double-buffered slots)")
     args = ap.parse_args()
     rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -47,39 +50,67 @@ def main():
     if plan.role(rank) == "moe":
         layer = MoELayer(rmap, d_h, d_e, T, k, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
-    box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local)
+    box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local, transport=args.transport)
     full = None
     if plan.role(rank) == "attention":
         full = MoELayer(rmap, d_h, d_e, T, k, instance=-1, device=local)
         full.set_weights(*build_weight_store(full, seed=1))
 
     stream = torch.cuda.current_stream(dev).cuda_stream
-    result = {"rank": rank, "role": plan.role(rank), "steps": []}
+    result = {"rank": rank, "role": plan.role(rank), "steps": [], "transport": box.transport}
+    steps = []
     for step in range(1, args.steps + 1):
         Ts = T - 37 * (step % 3)  # vary the step size: ragged shards
         b = J.gen_batch(J.RoutingPattern.gaussian(E, 0.2), Ts, k, 7, step)
         x, gw = make_inputs(Ts, k, d_h, step, dev)
         ex = torch.from_numpy(b.experts).to(dev)
-        if plan.role(rank) == "attention":
+        steps.append((Ts, x, gw, ex))
+
+    if plan.role(rank) == "attention":
+        outs = {}
+
+        def dispatch(step):
+            Ts, x, gw, ex = steps[step - 1]
             first, cnt = plan.shard(Ts, rank)
-            out = torch.empty(cnt, d_h, dtype=torch.bfloat16, device=dev)
-            box.dispatch(x[first:first + cnt].contiguous(), ex[first * k:(first + cnt) * k],
-                         gw[first * k:(first + cnt) * k], Ts, step, stream)
-            box.combine(out, Ts, step, stream)
+            box.dispatch(x[first:first + cnt].contiguous(), ex[first * k:(first + cnt) * k].contiguous(),
+                         gw[first * k:(first + cnt) * k].contiguous(), Ts, step, stream)
+
+        def combine(step):
+            Ts = steps[step - 1][0]
+            first, cnt = plan.shard(Ts, rank)
+            outs[step] = torch.empty(cnt, d_h, dtype=torch.bfloat16, device=dev)
+            box.combine(outs[step], Ts, step, stream)
+
+        if args.inflight == 1:
+            for step in range(1, args.steps + 1):
+                dispatch(step)
+                combine(step)
+                torch.cuda.synchronize()
+        else:
+            dispatch(1)
+            for step in range(1, args.steps + 1):
+                if step < args.steps:
+                    dispatch(step + 1)
+                combine(step)
+            torch.cuda.synchronize()
+        for step in range(1, args.steps + 1):
+            Ts, x, gw, ex = steps[step - 1]
+            first, cnt = plan.shard(Ts, rank)
             ref = full.forward(x, ex, gw)[first:first + cnt]
             torch.cuda.synchronize()
-            o, r = out.float().cpu().numpy(), ref.float().cpu().numpy()
+            o, r = outs[step].float().cpu().numpy(), ref.float().cpu().numpy()
             rms = float(np.sqrt(np.mean(r.astype(np.float64) ** 2))) or 1.0
             bad = int((np.abs(o - r) > RTOL * np.abs(r) + ATOL * rms).sum())
             result["steps"].append({"T": Ts, "shard": [first, cnt], "bad": bad,
                                     "max_err_over_rms": float(np.abs(o - r).max() / rms)})
-        else:
-            box.moe_step(Ts, step, stream)
-            torch.cuda.synchronize()
-            result["steps"].append({"T": Ts})
+    else:
+        for step in range(1, args.steps + 1):
+            box.moe_step(steps[step - 1][0], step, stream)
+            result["steps"].append({"T": steps[step - 1][0]})
+        torch.cuda.synchronize()
     result["timed_out"] = box.timed_out()
     os.makedirs(args.out, exist_ok=True)
-    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_rank{rank}.json"), "w") as f:
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}_rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
     dist.destroy_process_group()

@@ -18,21 +18,25 @@ def gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+@pytest.mark.parametrize("transport,inflight", [("p2p", 1), ("p2p", 2), ("nvls", 1), ("nvls", 2)])
 @pytest.mark.parametrize("attn,moe", [(1, 1), (1, 3), (2, 2)])
-def test_box_exchange_matches_single_gpu_layer(attn, moe):
+def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
     if gpus() < attn + moe:
         pytest.skip(f"needs {attn + moe} GPUs (one rank per GPU)")
     out = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={attn + moe}", "--master-addr", "127.0.0.1", "--master-port",
-           str(29500 + 10 * attn + moe), os.path.join(ROOT, "tests", "dist_worker.py"),
-           "--attn", str(attn), "--moe", str(moe), "--out", out]
+           str(29500 + 10 * attn + moe + (50 if transport == "nvls" else 0) + 100 * inflight),
+           os.path.join(ROOT, "tests", "dist_worker.py"),
+           "--attn", str(attn), "--moe", str(moe), "--out", out, "--transport", transport,
+           "--inflight", str(inflight)]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
     assert len(res) == attn + moe
     for r in res:
         assert not r["timed_out"], r
+        assert r["transport"] == transport
         if r["role"] == "attention":
             for s in r["steps"]:
                 assert s["bad"] == 0, s
