@@ -257,13 +257,20 @@ struct TileCoord {
 __device__ __forceinline__ int rows_per_cta(int rows) { return (((rows + 1) >> 1) + 7) & ~7; }
 
 // Tile t (relative to the first tile of q_begin) -> (group, m-block, rows).
-// Group-major, n-tiles fastest (consecutive tiles share the weight block).  A
+// Group-major, n-tiles fastest (consecutive tiles share the weight block),
+// walked zig-zag (below).  A
 // group of r rows has max(1, r / tile_n) tiles; the last one also takes the
 // remainder, so it can hold up to 2*tile_n - 1 rows ("wide": two sub-tiles
 // that share every weight k-block) — a remainder never costs its own pass over
 // the weights.
-__device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t) {
+__device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in) {
   const int base = p.tile_off[p.q_begin];
+  // draws alternate between the front and the back of the list: replica order
+  // follows placement order (hot experts first, experts.cpp place_replicas), so
+  // tensor-bound hot tiles and weight-streaming cold tiles run side by side
+  // (c2, T=4096: 334 -> 329 us)
+  const int total = (p.tile_off[p.q_end] - base) * p.m_tiles;
+  const int t = (t_in & 1) ? total - 1 - (t_in >> 1) : (t_in >> 1);
   int lo = p.q_begin, hi = p.q_end;  // find q: (tile_off[q]-base)*m <= t < (tile_off[q+1]-base)*m
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
