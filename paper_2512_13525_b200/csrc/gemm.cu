@@ -258,11 +258,11 @@ __device__ __forceinline__ int rows_per_cta(int rows) { return (((rows + 1) >> 1
 
 // Tile t (relative to the first tile of q_begin) -> (group, m-block, rows).
 // Group-major, n-tiles fastest (consecutive tiles share the weight block),
-// walked zig-zag (below).  A
-// group of r rows has max(1, r / tile_n) tiles; the last one also takes the
-// remainder, so it can hold up to 2*tile_n - 1 rows ("wide": two sub-tiles
-// that share every weight k-block) — a remainder never costs its own pass over
-// the weights.
+// walked zig-zag (below).  The n-tile count per group comes from K2
+// (tile_off): ceil(r / tile_n), or in decode (merge_tail) max(1, r / tile_n)
+// with the last tile also taking the remainder — up to 2*tile_n - 1 rows, a
+// "wide" tile of two sub-tiles sharing every weight k-block, so a remainder
+// never costs its own pass over the weights.
 __device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in) {
   const int base = p.tile_off[p.q_begin];
   // draws alternate between the front and the back of the list: replica order
