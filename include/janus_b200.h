@@ -147,6 +147,25 @@ janus_status janus_profile_read(janus_ctx *ctx, double *sched_ms, double *ffn_ms
 janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int num_tokens,
                                   int top_k, int64_t *ns);
 
+/* ---- MoE-side gating ------------------------------------ */
+/* Janus gates on the MoE side; the reference only consumes
+ * top-k ids (ActivationBatch, aebs.hpp:15-24).  device: logits = x · Wrᵀ
+ * (x [T][d_h] bf16, Wr [E][d_h] bf16, fp32 accumulation on tcgen05), top-k ids
+ * by descending logit — ties to the lower id — into experts [T*k] in rank
+ * order, softmax of the k selected logits into gate_w [T*k].
+ * Needs d_h % 64 == 0, E % 16 == 0, 16 <= E <= 256, 1 <= k <= min(16, E). */
+janus_status janus_gate_async(janus_ctx *ctx, const void *d_x, const void *d_router, int64_t T,
+                              int d_hidden, int num_experts, int top_k, int32_t *d_experts,
+                              float *d_gate_w, void *stream);
+/* Router weights [E][d_h] bf16 for janus_moe_layer_gated_async (device
+ * pointer, caller-owned; E from the replica map, d_h / k from
+ * janus_moe_configure). */
+janus_status janus_moe_set_router(janus_ctx *ctx, const void *d_router);
+/* device: the gating kernel on this GPU, then janus_moe_layer_async on its
+ * ids and weights (kept in the context's workspace). */
+janus_status janus_moe_layer_gated_async(janus_ctx *ctx, const void *d_x, int num_tokens,
+                                         void *d_out, void *stream);
+
 /* ---- attention <-> MoE exchange (one NVLink box) ------------------------ */
 /* Token ownership on the attention side: even split, remainder to the lowest
  * ids (comm.cpp:76-81).  Writes first token and count of shard a. */

@@ -630,6 +630,48 @@ void or_combine(const float *y, const int32_t *slot_row, const float *w, int T, 
   }
 }
 
+/* MoE-side gating (no reference implementation — Janus gates
+ * on the MoE side, the reference only consumes top-k ids):
+ *   logits[t][e] = x[t]·Wr[e] (bf16 inputs, accumulated in double here),
+ *   top-k by logit descending, ties to the lower expert id (out order = rank),
+ *   gate weights = softmax over the k selected logits (Qwen3-MoE's
+ *   norm_topk_prob form).
+ * x: [T, d_h] bf16; wr: [E, d_h] bf16; experts/gw: [T*k]; logits_out
+ * (optional) [T, E] as double. */
+void or_gate(const uint16_t *x, const uint16_t *wr, int T, int d_h, int E, int k,
+             int32_t *experts, float *gw, double *logits_out) {
+  double *lg = (double *)malloc(sizeof(double) * (E > 0 ? E : 1));
+  double *wf = (double *)malloc(sizeof(double) * (size_t)E * d_h);
+  for (long long i = 0; i < (long long)E * d_h; ++i) wf[i] = bf16_to_f32(wr[i]);
+  double *xf = (double *)malloc(sizeof(double) * (d_h > 0 ? d_h : 1));
+  for (int t = 0; t < T; ++t) {
+    for (int i = 0; i < d_h; ++i) xf[i] = bf16_to_f32(x[(size_t)t * d_h + i]);
+    for (int e = 0; e < E; ++e) {
+      const double *w = wf + (size_t)e * d_h;
+      double acc = 0;
+      for (int i = 0; i < d_h; ++i) acc += w[i] * xf[i];
+      lg[e] = acc;
+      if (logits_out) logits_out[(size_t)t * E + e] = acc;
+    }
+    int32_t *ex = experts + (size_t)t * k;
+    for (int j = 0; j < k; ++j) {  /* selection: largest remaining, lowest id on ties */
+      int best = -1;
+      for (int e = 0; e < E; ++e) {
+        int taken = 0;
+        for (int q = 0; q < j; ++q) taken |= ex[q] == e;
+        if (!taken && (best < 0 || lg[e] > lg[best])) best = e;
+      }
+      ex[j] = best;
+    }
+    double m = lg[ex[0]], sum = 0;
+    for (int j = 0; j < k; ++j) sum += exp(lg[ex[j]] - m);
+    for (int j = 0; j < k; ++j) gw[(size_t)t * k + j] = (float)(exp(lg[ex[j]] - m) / sum);
+  }
+  free(lg);
+  free(wf);
+  free(xf);
+}
+
 int or_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -116,6 +116,8 @@ class Oracle:
                                        C.c_int, f32p]
         L.or_combine.argtypes = [f32p, i32p, f32p, C.c_int, C.c_int, C.c_int, f32p]
         L.or_f32_to_bf16.argtypes = [f32p, u16p, C.c_longlong]
+        L.or_gate.argtypes = [u16p, u16p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f32p,
+                              C.c_void_p]
         L.or_num_threads.restype = C.c_int
 
     # --- rng / routing ------------------------------------------------------
@@ -204,6 +206,18 @@ class Oracle:
                           np.ascontiguousarray(slot_row, np.int32),
                           np.ascontiguousarray(w, np.float32), T, k, d_h, out)
         return out
+
+    def gate(self, x_bf16, wr_bf16, k, want_logits=False):
+        """Router logits (double), top-k ids by descending logit (ties: lower
+        id), softmax over the selected — the gating definition (§8(f) 1)."""
+        T, d_h = x_bf16.shape
+        E = wr_bf16.shape[0]
+        ex = np.zeros(T * k, np.int32)
+        gw = np.zeros(T * k, np.float32)
+        lg = np.zeros((T, E), np.float64) if want_logits else None
+        self.L.or_gate(np.ascontiguousarray(x_bf16), np.ascontiguousarray(wr_bf16), T, d_h, E, k,
+                       ex, gw, lg.ctypes.data if want_logits else None)
+        return (ex, gw, lg) if want_logits else (ex, gw)
 
     def f32_to_bf16(self, a: np.ndarray) -> np.ndarray:
         a = np.ascontiguousarray(a, np.float32)

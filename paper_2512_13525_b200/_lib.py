@@ -27,7 +27,8 @@ SYMBOLS = (
     "janus_profile_read", "janus_trace_schedule", "janus_xfer_configure", "janus_xfer_handle",
     "janus_xfer_connect", "janus_attn_dispatch_async", "janus_moe_layer_xfer_async",
     "janus_attn_combine_async", "janus_xfer_status", "janus_xfer_mc_supported",
-    "janus_xfer_mc_create", "janus_xfer_mc_join", "janus_xfer_mc_bind",
+    "janus_xfer_mc_create", "janus_xfer_mc_join", "janus_xfer_mc_bind", "janus_gate_async",
+    "janus_moe_set_router", "janus_moe_layer_gated_async",
 )
 
 
@@ -81,6 +82,9 @@ def _load() -> C.CDLL:
     L.janus_xfer_mc_create.argtypes = [vp, P(i32)]
     L.janus_xfer_mc_join.argtypes = [vp, i32]
     L.janus_xfer_mc_bind.argtypes = [vp]
+    L.janus_gate_async.argtypes = [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp]
+    L.janus_moe_set_router.argtypes = [vp, vp]
+    L.janus_moe_layer_gated_async.argtypes = [vp, vp, i32, vp, vp]
     return L
 
 

@@ -721,6 +721,44 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, ui
   return JANUS_OK;
 }
 
+janus_status janus_gate_async(janus_ctx *ctx, const void *d_x, const void *d_router, int64_t T,
+                              int d_hidden, int num_experts, int top_k, int32_t *d_experts,
+                              float *d_gate_w, void *stream) {
+  if (!ctx) return JANUS_EINVAL;
+  if (T < 0 || T > (1 << 26) || (T > 0 && (!d_x || !d_router || !d_experts || !d_gate_w)))
+    return fail(ctx, JANUS_EINVAL, "gate: bad arguments");
+  if (!janus::gate_shape_ok(d_hidden, num_experts, top_k))
+    return fail(ctx, JANUS_EUNSUPPORTED,
+                "gate: need d_hidden % 64 == 0, 16 <= num_experts <= 256, num_experts % 16 == 0, "
+                "1 <= top_k <= min(16, num_experts)");
+  CK(cudaSetDevice(ctx->device));
+  cudaError_t e = janus::launch_gate(d_x, d_router, (int)T, d_hidden, num_experts, top_k,
+                                     d_experts, d_gate_w, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gate_kernel");
+  if (T > 0) ctx->launches += 1;
+  return JANUS_OK;
+}
+
+janus_status janus_moe_set_router(janus_ctx *ctx, const void *d_router) {
+  if (!ctx) return JANUS_EINVAL;
+  if (!d_router) return fail(ctx, JANUS_EINVAL, "gate: null router");
+  ctx->router = d_router;
+  return JANUS_OK;
+}
+
+janus_status janus_moe_layer_gated_async(janus_ctx *ctx, const void *d_x, int T, void *d_out,
+                                         void *stream) {
+  if (!ctx) return JANUS_EINVAL;
+  if (!ctx->router) return fail(ctx, JANUS_ESTATE, "gate: janus_moe_set_router first");
+  if (!ctx->d_experts) return fail(ctx, JANUS_ESTATE, "moe: janus_moe_configure first");
+  if (T < 0 || T > ctx->max_tokens)
+    return fail(ctx, JANUS_EINVAL, "moe: num_tokens outside [0, max_tokens]");
+  janus_status st = janus_gate_async(ctx, d_x, ctx->router, T, ctx->d_h, ctx->dmap.E,
+                                     ctx->top_k, ctx->d_experts, ctx->d_gw, stream);
+  if (st != JANUS_OK) return st;
+  return janus_moe_layer_async(ctx, d_x, ctx->d_experts, ctx->d_gw, T, d_out, nullptr, stream);
+}
+
 janus_status janus_xfer_mc_supported(janus_ctx *ctx, int *yes) {
   if (!ctx || !yes) return JANUS_EINVAL;
   *yes = janus::mc_supported(ctx->device) ? 1 : 0;

@@ -33,9 +33,12 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace janus {
 namespace {
+
+using namespace sm100;
 
 constexpr int kBK = 64;                        // K elements per stage (128-B rows, SW128)
 constexpr int kATileBytes = 128 * kBK * 2;     // 16 KB: this CTA's 128 weight rows
@@ -81,10 +84,6 @@ struct GemmParams {
   int out_ld;     // elements per output row
 };
 
-// ---------------------------------------------------------------- PTX -----
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 // Cluster-window address of the same smem variable in CTA `rank` of the cluster.
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
   uint32_t r;
@@ -100,14 +99,6 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
 }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
 // Publish a 32-bit value into a CTA's smem and complete that CTA's mbarrier
 // phase with it (arrive + expect 4 bytes, then st.async completing them): no
 // release fence, so the issuing thread does not wait for its in-flight TMA.
@@ -120,32 +111,10 @@ __device__ __forceinline__ void publish_u32(uint32_t cl_dst, uint32_t v, uint32_
                "r"(v), "r"(cl_bar)
                : "memory");
 }
-// One lane of a converged warp.  The single-thread roles (TMA producers, MMA
-// issuer) run as whole warps and issue through elect_one(), so their loop
-// state stays warp-uniform and ptxas keeps TMA/UMMA operands in uniform
-// registers (no per-instruction R2UR waterfall as under `if (lane == 0)`).
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-               : "=r"(pred));
-  return pred != 0;
-}
 // Relaxed arrive (consumers of the tile queue: only "read before reuse").
 __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  uint32_t ok;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!ok);
 }
 // TMA 2-D tile load by either CTA of the pair; completion bytes are counted on
 // the leader CTA's mbarrier (cluster-window address).
@@ -166,33 +135,6 @@ __device__ __forceinline__ void tma_load_pair_4d(void *dst, const CUtensorMap *t
       ".L2::cache_hint [%0], [%1, {%2, %3, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x0), "r"(0), "r"(x3), "r"(bar_leader), "l"(policy)
       : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-// SW128 K-major smem matrix descriptor (cute::UMMA::SmemDescriptor layout):
-// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4
-// [32,46) = 1024 B between 8-row groups, version 1 [46,48), layout 2 = 128B
-// swizzle [61,64).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=256 (pair).
 __device__ __forceinline__ uint32_t idesc_bf16_m256(int n) {
@@ -228,10 +170,6 @@ __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t *>(&v);
-}
 // Four 8x8 b16 matrices from mma-fragment registers, stored transposed: lane l
 // supplies the smem address of row l%8 of matrix l/8.
 __device__ __forceinline__ void stmatrix_x4_trans(uint32_t addr, uint32_t a0, uint32_t a1,
@@ -692,37 +630,8 @@ int sm_count() {
   return n;
 }
 
-using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                              const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                              const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-EncodeFn encode_fn() {
-  static EncodeFn fn = nullptr;
-  if (!fn) {
-    void *ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(ptr);
-  }
-  return fn;
-}
 
-// 2-D bf16 row-major [rows][cols] tensor map, box {64, box_rows}, 128B swizzle.
-bool make_map(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-  EncodeFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 // Epilogue output map: bf16 [rows][cols], no swizzle, box {box_cols, 32 rows}.
 bool make_out_map(CUtensorMap *tm, const void *base, uint64_t rows, uint64_t cols,

@@ -71,6 +71,11 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
                            cudaStream_t s);
 
+// MoE-side gating (gate.cu): router GEMM + top-k + softmax of the top-k logits.
+bool gate_shape_ok(int d_h, int E, int k);
+cudaError_t launch_gate(const void *x, const void *wr, int T, int d_h, int E, int k,
+                        int32_t *experts, float *gw, cudaStream_t s);
+
 // Attention <-> MoE exchange (xfer.cu).  Ranks [0, A) own token shards,
 // ranks [A, A+M) are MoE instances g = rank - A.  One exchange region per
 // rank, identical layout everywhere.
@@ -152,6 +157,7 @@ struct janus_ctx {
   void *d_x = nullptr, *d_outbuf = nullptr;
   int32_t *d_experts = nullptr;
   float *d_gw = nullptr;
+  const void *router = nullptr;  // [E][d_h] bf16 (janus_moe_set_router; caller-owned)
 
   // CUDA-graph replay of the single-GPU layer (janus_moe_layer_async)
   struct GraphKey {

@@ -96,6 +96,42 @@ class MoELayer:
             raise JanusError(st, self.sched.last_error())
         return out
 
+    # --- MoE-side gating ----------------------------------------
+    def set_router(self, wr: torch.Tensor) -> None:
+        """Router weights [E][d_h] bf16 for :meth:`forward_gated`."""
+        assert wr.shape == (self.map.num_experts, self.d_h) and wr.dtype == torch.bfloat16
+        assert wr.is_cuda and wr.is_contiguous()
+        self.wr = wr  # keep alive: the context stores the raw pointer
+        st = lib.janus_moe_set_router(self.ctx, wr.data_ptr())
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+
+    def gate(self, x: torch.Tensor, wr: torch.Tensor | None = None, top_k: int | None = None):
+        """(experts int32 [T*k], gate_w fp32 [T*k]) from the gating kernel."""
+        wr = self.wr if wr is None else wr
+        k = self.k if top_k is None else top_k
+        T = x.shape[0]
+        ex = torch.empty(T * k, dtype=torch.int32, device=x.device)
+        gw = torch.empty(T * k, dtype=torch.float32, device=x.device)
+        st = lib.janus_gate_async(self.ctx, x.data_ptr(), wr.data_ptr(), T, x.shape[1],
+                                  wr.shape[0], k, ex.data_ptr(), gw.data_ptr(),
+                                  _cur_stream(self.device))
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+        return ex, gw
+
+    def forward_gated(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Gate on this GPU, then the layer (device call, current stream)."""
+        T = x.shape[0]
+        assert x.dtype == torch.bfloat16 and x.shape[1] == self.d_h and x.is_contiguous()
+        if out is None:
+            out = torch.empty_like(x)
+        st = lib.janus_moe_layer_gated_async(self.ctx, x.data_ptr(), T, out.data_ptr(),
+                                             _cur_stream(self.device))
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+        return out
+
     def launches(self) -> int:
         return self.sched.launches()
 
@@ -127,6 +163,14 @@ def build_weight_store(layer: MoELayer, seed: int) -> tuple:
         w13[q, layer.d_e:] = wu
         w2[q] = wd
     return w13, w2
+
+
+def router_weights(E: int, d_h: int, seed: int, device) -> torch.Tensor:
+    """Random-init router [E][d_h] bf16, N(0, 1/sqrt(d_h)), seeded by
+    derive_seed(seed, "router", E)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(derive_seed(seed, "router", E) & ((1 << 63) - 1))
+    return (torch.randn(E, d_h, generator=g, device=device) * (d_h ** -0.5)).bfloat16()
 
 
 def make_inputs(T: int, k: int, d_h: int, seed: int, device) -> tuple:
