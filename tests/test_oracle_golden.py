@@ -152,3 +152,26 @@ def test_dispatch_layout_definition(oracle):
     # keys non-decreasing along rows
     keys = [(a.instance[s], int(a.replica[s]), int(ex[s]), s) for s in row_slot]
     assert keys == sorted(keys)
+
+
+def test_gate_definition(oracle):
+    """or_gate (§8(f) 1) against a numpy restatement: logits in float64 over
+    the bf16 inputs, top-k by (logit desc, id asc), softmax of the selected."""
+    rng = np.random.default_rng(3)
+    T, d_h, E, k = 40, 64, 32, 4
+    x = rng.standard_normal((T, d_h)).astype(np.float32)
+    w = (rng.standard_normal((E, d_h)) / 8).astype(np.float32)
+    w[5] = w[9]  # an exact tie: experts 5 and 9 always share a logit
+    xb, wb = oracle.f32_to_bf16(x), oracle.f32_to_bf16(w)
+    ex, gw, lg = oracle.gate(xb, wb, k, want_logits=True)
+    xf = (xb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    wf = (wb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    ref = xf @ wf.T
+    np.testing.assert_allclose(lg, ref, rtol=1e-12, atol=1e-12)
+    for t in range(T):
+        order = sorted(range(E), key=lambda e: (-ref[t, e], e))[:k]
+        assert list(ex[t * k:(t + 1) * k]) == order
+        z = np.exp(ref[t, order] - ref[t, order[0]])
+        np.testing.assert_allclose(gw[t * k:(t + 1) * k], z / z.sum(), rtol=1e-6)
+        if 5 in order and 9 in order:
+            assert order.index(5) < order.index(9)
