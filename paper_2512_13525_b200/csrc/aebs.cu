@@ -194,6 +194,9 @@ struct Slots<0> {
 template <int MAXIT>
 __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  // the layer's next kernel (K3, launched with PDL) may become resident now;
+  // it waits for this grid's completion before reading the layout
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   cg::cluster_group cluster = cg::this_cluster();
   const int crank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
   const int E = a.map.E, N = a.map.N, R = a.map.R, S = a.S;

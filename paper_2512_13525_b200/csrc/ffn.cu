@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace janus {
 namespace {
@@ -35,6 +36,8 @@ constexpr int kWarpsPerBlock = 4;
 __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__restrict__ slot_row,
                                const int32_t *__restrict__ slot_inst, int instance, int T, int k,
                                int vec, uint4 *__restrict__ xp) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();  // slot_row / slot_inst from K1
   const int lane = threadIdx.x & 31;
   const int segs = (vec + 32 * kPermU - 1) / (32 * kPermU);
   const int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -85,6 +88,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
     combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
                    const int32_t *__restrict__ slot_inst, int instance,
                    const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();  // y from the down GEMM
   const int lane = threadIdx.x & 31;
   const int segs = (vec + 32 * kCombU - 1) / (32 * kCombU);
   const int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -171,10 +176,9 @@ cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t
   const int T = S / k, vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kPermU - 1) / (32 * kPermU));
   const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  permute_kernel<<<blocks, 32 * kWarpsPerBlock, 0, s>>>(reinterpret_cast<const uint4 *>(x),
-                                                        slot_row, slot_instance, instance, T, k,
-                                                        vec, reinterpret_cast<uint4 *>(xp));
-  return cudaGetLastError();
+  return sm100::launch_pdl(permute_kernel, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
+                           reinterpret_cast<const uint4 *>(x), slot_row, slot_instance, instance,
+                           T, k, vec, reinterpret_cast<uint4 *>(xp));
 }
 
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
@@ -184,10 +188,9 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
   const int vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kCombU - 1) / (32 * kCombU));
   const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  combine_kernel<4><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(
-      reinterpret_cast<const uint4 *>(y), slot_row, slot_instance, instance, gate_w, T, k, vec,
-      reinterpret_cast<uint4 *>(out));
-  return cudaGetLastError();
+  return sm100::launch_pdl(combine_kernel<4>, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
+                           reinterpret_cast<const uint4 *>(y), slot_row, slot_instance, instance,
+                           gate_w, T, k, vec, reinterpret_cast<uint4 *>(out));
 }
 
 }  // namespace janus

@@ -257,7 +257,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
   const bool leader = crank == 0;
-  const int total = (p.tile_off[p.q_end] - p.tile_off[p.q_begin]) * p.m_tiles;
   const int kblocks = p.K / kBK;
 
   if (warp == 0 && lane == 0) {
@@ -287,6 +286,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
+  pdl_wait();  // token rows (K3 / the gate-up GEMM) and the tile list (K1): read below only
+  const int total = (p.tile_off[p.q_end] - p.tile_off[p.q_begin]) * p.m_tiles;
 
   // Dynamic tile scheduler: the leader's producer takes tile indices from a
   // global counter (one tile ahead) and publishes each through a kTQ-slot
@@ -696,8 +698,8 @@ cudaError_t launch_gemm(const GemmParams &g, cudaStream_t s) {
     configured_dev = dev;
   }
   const int grid = sm_count() & ~1;  // CTA pairs
-  grouped_gemm_kernel<MODE, BH><<<grid, kGemmThreads, Ring<BH>::kSmemBytes, s>>>(g);
-  return cudaGetLastError();
+  return launch_pdl(grouped_gemm_kernel<MODE, BH>, dim3(grid), dim3(kGemmThreads),
+                    Ring<BH>::kSmemBytes, s, g);
 }
 
 }  // namespace
