@@ -166,6 +166,25 @@ janus_status janus_moe_set_router(janus_ctx *ctx, const void *d_router);
 janus_status janus_moe_layer_gated_async(janus_ctx *ctx, const void *d_x, int num_tokens,
                                          void *d_out, void *stream);
 
+/* ---- activation statistics ------------------------------ */
+/* ActivationStats (experts.hpp:18-43, experts.cpp:11-62) on the device:
+ * per-expert activation counts and the symmetric co-activation matrix over the
+ * last `window` steps.  Configure allocates and zeroes the state (errors as
+ * the reference's constructor). */
+janus_status janus_stats_configure(janus_ctx *ctx, int num_experts, int window);
+/* device: record_step for the activated set of one step's routing (the
+ * distinct ids of experts[T*k]).  An id outside [0, E) rejects the step (state
+ * unchanged, janus_stats_status reports it) — the reference's
+ * "stats: activated expert X out of range". */
+janus_status janus_stats_record_async(janus_ctx *ctx, const int32_t *d_experts, int64_t num_tokens,
+                                      int top_k, void *stream);
+/* host (synchronises the context's device): counts [E], coact [E*E] (zero
+ * diagonal), steps recorded in the window (reference recorded_steps()). */
+janus_status janus_stats_read(janus_ctx *ctx, int64_t *counts, int64_t *coact, int *recorded);
+/* host: the last recorded step's verdict: JANUS_OK, or JANUS_EINVAL with the
+ * reference message in janus_last_error (bad_expert = the offending id). */
+janus_status janus_stats_status(janus_ctx *ctx, int *bad_expert);
+
 /* ---- attention <-> MoE exchange (one NVLink box) ------------------------ */
 /* Token ownership on the attention side: even split, remainder to the lowest
  * ids (comm.cpp:76-81).  Writes first token and count of shard a. */

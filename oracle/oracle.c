@@ -672,6 +672,38 @@ void or_gate(const uint16_t *x, const uint16_t *wr, int T, int d_h, int E, int k
   free(xf);
 }
 
+/* ActivationStats::record_step (experts.cpp:30-57), restated over a ring of
+ * the last `window` activated sets kept as bitmasks (the device layout):
+ * counts[e] = #steps in the window with e activated, coact[i][j] (i != j) =
+ * #steps with both.  `ring` holds window * words uint32 (words = ceil(E/32)),
+ * `step` the number of steps recorded before this one.  Returns 0, or 1 + the
+ * first bad index if the set is not ascending/distinct/in range (the
+ * reference's ValidationError cases). */
+int or_stats_record(int E, int window, long long step, uint32_t *ring, long long *counts,
+                    long long *coact, const int32_t *activated, int n) {
+  const int words = (E + 31) / 32;
+  for (int i = 0; i < n; ++i)
+    if (activated[i] < 0 || activated[i] >= E || (i > 0 && activated[i - 1] >= activated[i]))
+      return 1 + i;
+  uint32_t *slot = ring + (size_t)(step % window) * words;
+  if (step >= window) { /* retire the oldest step, which lives in this slot */
+    for (int i = 0; i < E; ++i) {
+      if (!((slot[i >> 5] >> (i & 31)) & 1u)) continue;
+      --counts[i];
+      for (int j = 0; j < E; ++j)
+        if (j != i && ((slot[j >> 5] >> (j & 31)) & 1u)) --coact[(size_t)i * E + j];
+    }
+  }
+  memset(slot, 0, sizeof(uint32_t) * words);
+  for (int i = 0; i < n; ++i) slot[activated[i] >> 5] |= 1u << (activated[i] & 31);
+  for (int i = 0; i < n; ++i) {
+    ++counts[activated[i]];
+    for (int j = 0; j < n; ++j)
+      if (j != i) ++coact[(size_t)activated[i] * E + activated[j]];
+  }
+  return 0;
+}
+
 int or_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -27,6 +27,7 @@ i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 
 POLICY_AEBS, POLICY_RANDOM, POLICY_BRUTE = 0, 1, 2
 OK, EINVAL, EUNKNOWN_EXPERT, EINFEASIBLE = 0, 1, 2, 3
@@ -116,6 +117,8 @@ class Oracle:
                                        C.c_int, f32p]
         L.or_combine.argtypes = [f32p, i32p, f32p, C.c_int, C.c_int, C.c_int, f32p]
         L.or_f32_to_bf16.argtypes = [f32p, u16p, C.c_longlong]
+        L.or_stats_record.argtypes = [C.c_int, C.c_int, C.c_longlong, u32p, i64p, i64p, i32p,
+                                      C.c_int]
         L.or_gate.argtypes = [u16p, u16p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f32p,
                               C.c_void_p]
         L.or_num_threads.restype = C.c_int
@@ -207,6 +210,20 @@ class Oracle:
                           np.ascontiguousarray(w, np.float32), T, k, d_h, out)
         return out
 
+    def stats_new(self, E, window):
+        """ActivationStats restatement state: (E, window, step, ring, counts, coact)."""
+        words = (E + 31) // 32
+        return {"E": E, "W": window, "step": 0, "ring": np.zeros(window * words, np.uint32),
+                "counts": np.zeros(E, np.int64), "coact": np.zeros(E * E, np.int64)}
+
+    def stats_record(self, st, activated):
+        a = np.ascontiguousarray(activated, np.int32)
+        r = self.L.or_stats_record(st["E"], st["W"], st["step"], st["ring"], st["counts"],
+                                   st["coact"], a, len(a))
+        if r:
+            raise ValueError(f"stats: bad activated set at {r - 1}")
+        st["step"] += 1
+
     def gate(self, x_bf16, wr_bf16, k, want_logits=False):
         """Router logits (double), top-k ids by descending logit (ties: lower
         id), softmax over the selected — the gating definition (§8(f) 1)."""
@@ -258,6 +275,11 @@ class Ref:
                                         C.c_int, C.POINTER(C.c_longlong)]
         L.ref_placement.argtypes = [C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int, C.c_int,
                                     C.c_int, C.c_int, C.c_int, C.c_uint64, i32p, i32p, i32p]
+        L.ref_stats_new.restype = C.c_void_p
+        L.ref_stats_new.argtypes = [C.c_int, C.c_int]
+        L.ref_stats_free.argtypes = [C.c_void_p]
+        L.ref_stats_record.argtypes = [C.c_void_p, i32p, C.c_int]
+        L.ref_stats_read.argtypes = [C.c_void_p, i64p, i64p]
         L.ref_moe_layer_latency.restype = C.c_double
         L.ref_moe_layer_latency.argtypes = [C.c_int, i32p, i64p, C.c_int, C.c_int, C.c_int,
                                             C.c_double, C.c_double, C.c_double]
@@ -328,6 +350,25 @@ class Ref:
             raise ValueError(self.err())
         R = int(off[-1])
         return CSRMap(E, N, C_, off, hosts[:R].copy(), rid[:R].copy())
+
+    def stats(self, E, window, steps):
+        """The reference ActivationStats fed `steps` (lists of activated ids):
+        (counts [E], coact [E*E]); raises ValueError with the reference's
+        message on a rejected step."""
+        h = self.L.ref_stats_new(E, window)
+        if not h:
+            raise ValueError(self.err())
+        try:
+            for a in steps:
+                a = np.ascontiguousarray(a, np.int32)
+                if self.L.ref_stats_record(h, a, len(a)):
+                    raise ValueError(self.err())
+            counts = np.zeros(E, np.int64)
+            coact = np.zeros(E * E, np.int64)
+            self.L.ref_stats_read(h, counts, coact)
+            return counts, coact
+        finally:
+            self.L.ref_stats_free(h)
 
     def moe_layer_latency(self, load, routed, d_h, d_e, bpp=2, peak_flops=1401.8e12,
                           hbm_bw=6372.5e9, t_launch=5e-6):

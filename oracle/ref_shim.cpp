@@ -275,4 +275,33 @@ int ref_dump_assignment(const int32_t* experts, int T, int k, int N, const int32
   return 0;
 }
 
+// ActivationStats (experts.cpp:11-62): windowed per-expert counts and the
+// co-activation matrix.  Opaque handle; status 1 = ValidationError (message
+// in ref_last_error).
+void* ref_stats_new(int E, int window) {
+  try {
+    return new ActivationStats(E, window);
+  } catch (const std::exception& e) {
+    fail(e, 1);
+    return nullptr;
+  }
+}
+void ref_stats_free(void* h) { delete static_cast<ActivationStats*>(h); }
+int ref_stats_record(void* h, const int32_t* activated, int n) {
+  try {
+    static_cast<ActivationStats*>(h)->record_step(std::vector<int32_t>(activated, activated + n));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+void ref_stats_read(void* h, long long* counts, long long* coact) {
+  auto* s = static_cast<ActivationStats*>(h);
+  const int E = s->num_experts();
+  for (int i = 0; i < E; ++i) {
+    counts[i] = s->count(i);
+    for (int j = 0; j < E; ++j) coact[static_cast<size_t>(i) * E + j] = s->coactivation(i, j);
+  }
+}
+
 }  // extern "C"

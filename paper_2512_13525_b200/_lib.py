@@ -28,7 +28,8 @@ SYMBOLS = (
     "janus_xfer_connect", "janus_attn_dispatch_async", "janus_moe_layer_xfer_async",
     "janus_attn_combine_async", "janus_xfer_status", "janus_xfer_mc_supported",
     "janus_xfer_mc_create", "janus_xfer_mc_join", "janus_xfer_mc_bind", "janus_gate_async",
-    "janus_moe_set_router", "janus_moe_layer_gated_async",
+    "janus_moe_set_router", "janus_moe_layer_gated_async", "janus_stats_configure",
+    "janus_stats_record_async", "janus_stats_read", "janus_stats_status",
 )
 
 
@@ -85,6 +86,10 @@ def _load() -> C.CDLL:
     L.janus_gate_async.argtypes = [vp, vp, vp, i64, i32, i32, i32, vp, vp, vp]
     L.janus_moe_set_router.argtypes = [vp, vp]
     L.janus_moe_layer_gated_async.argtypes = [vp, vp, i32, vp, vp]
+    L.janus_stats_configure.argtypes = [vp, i32, i32]
+    L.janus_stats_record_async.argtypes = [vp, vp, i64, i32, vp]
+    L.janus_stats_read.argtypes = [vp, P(i64), P(i64), P(i32)]
+    L.janus_stats_status.argtypes = [vp, P(i32)]
     return L
 
 

@@ -2,6 +2,7 @@
 // validation, scheduling, MoE layer orchestration.  Host code only; kernels
 // live in aebs.cu / ffn.cu.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -135,6 +136,8 @@ janus_status janus_create(janus_ctx **out, int device) {
   return JANUS_OK;
 }
 
+static void free_stats(janus::StatsState &st);
+
 void janus_destroy(janus_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
@@ -156,6 +159,7 @@ void janus_destroy(janus_ctx *ctx) {
   for (auto &g : ctx->graphs) cudaGraphExecDestroy(g.exec);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   janus::mc_free(ctx->xfer, ctx->device);
+  free_stats(ctx->stats);
   for (void *p : ctx->xfer.opened) cudaIpcCloseMemHandle(p);
   dfree(ctx->xfer.local);
   dfree(ctx->xfer.counter);
@@ -757,6 +761,86 @@ janus_status janus_moe_layer_gated_async(janus_ctx *ctx, const void *d_x, int T,
                                      ctx->top_k, ctx->d_experts, ctx->d_gw, stream);
   if (st != JANUS_OK) return st;
   return janus_moe_layer_async(ctx, d_x, ctx->d_experts, ctx->d_gw, T, d_out, nullptr, stream);
+}
+
+static void free_stats(janus::StatsState &st) {
+  dfree(st.counts);
+  dfree(st.coact);
+  dfree(st.ring);
+  dfree(st.mask);
+  dfree(st.step);
+  dfree(st.bad);
+  st = janus::StatsState{};
+}
+
+janus_status janus_stats_configure(janus_ctx *ctx, int num_experts, int window) {
+  if (!ctx) return JANUS_EINVAL;
+  if (num_experts <= 0) return fail(ctx, JANUS_EINVAL, "stats: num_experts must be > 0");
+  if (window <= 0) return fail(ctx, JANUS_EINVAL, "stats: window must be > 0");
+  if (num_experts > JANUS_MAX_EXPERTS)
+    return fail(ctx, JANUS_EUNSUPPORTED, "stats: at most JANUS_MAX_EXPERTS experts");
+  CK(cudaSetDevice(ctx->device));
+  janus::StatsState &st = ctx->stats;
+  free_stats(st);
+  const int words = (num_experts + 31) / 32;
+  st.E = num_experts;
+  st.W = window;
+  CK(dalloc(&st.counts, num_experts));
+  CK(dalloc(&st.coact, (size_t)num_experts * num_experts));
+  CK(dalloc(&st.ring, (size_t)window * words));
+  CK(dalloc(&st.mask, words));
+  CK(dalloc(&st.step, 1));
+  CK(dalloc(&st.bad, 1));
+  CK(cudaMemset(st.counts, 0, sizeof(long long) * num_experts));
+  CK(cudaMemset(st.coact, 0, sizeof(long long) * num_experts * num_experts));
+  CK(cudaMemset(st.ring, 0, sizeof(uint32_t) * window * words));
+  CK(cudaMemset(st.step, 0, sizeof(long long)));
+  const int none = INT_MAX;
+  CK(cudaMemcpy(st.bad, &none, sizeof(int), cudaMemcpyHostToDevice));
+  return JANUS_OK;
+}
+
+janus_status janus_stats_record_async(janus_ctx *ctx, const int32_t *d_experts, int64_t T,
+                                      int top_k, void *stream) {
+  if (!ctx) return JANUS_EINVAL;
+  if (!ctx->stats.counts) return fail(ctx, JANUS_ESTATE, "stats: janus_stats_configure first");
+  if (T < 0 || top_k < 1 || (T > 0 && !d_experts))
+    return fail(ctx, JANUS_EINVAL, "stats: bad batch");
+  cudaError_t e = janus::launch_stats_record(ctx->stats, d_experts, T * top_k,
+                                             static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "stats kernels");
+  ctx->launches += 3;
+  return JANUS_OK;
+}
+
+janus_status janus_stats_read(janus_ctx *ctx, int64_t *counts, int64_t *coact, int *recorded) {
+  if (!ctx) return JANUS_EINVAL;
+  const janus::StatsState &st = ctx->stats;
+  if (!st.counts) return fail(ctx, JANUS_ESTATE, "stats: janus_stats_configure first");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  if (counts) CK(cudaMemcpy(counts, st.counts, sizeof(int64_t) * st.E, cudaMemcpyDeviceToHost));
+  if (coact)
+    CK(cudaMemcpy(coact, st.coact, sizeof(int64_t) * st.E * st.E, cudaMemcpyDeviceToHost));
+  if (recorded) {
+    long long step = 0;
+    CK(cudaMemcpy(&step, st.step, sizeof(long long), cudaMemcpyDeviceToHost));
+    *recorded = (int)std::min<long long>(step, st.W);
+  }
+  return JANUS_OK;
+}
+
+janus_status janus_stats_status(janus_ctx *ctx, int *bad_expert) {
+  if (!ctx) return JANUS_EINVAL;
+  if (!ctx->stats.bad) return fail(ctx, JANUS_ESTATE, "stats: janus_stats_configure first");
+  CK(cudaSetDevice(ctx->device));
+  int bad = INT_MAX;
+  CK(cudaMemcpy(&bad, ctx->stats.bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad_expert) *bad_expert = bad == INT_MAX ? -1 : bad;
+  if (bad != INT_MAX)
+    return fail(ctx, JANUS_EINVAL,
+                "stats: activated expert " + std::to_string(bad) + " out of range");
+  return JANUS_OK;
 }
 
 janus_status janus_xfer_mc_supported(janus_ctx *ctx, int *yes) {

@@ -76,6 +76,19 @@ bool gate_shape_ok(int d_h, int E, int k);
 cudaError_t launch_gate(const void *x, const void *wr, int T, int d_h, int E, int k,
                         int32_t *experts, float *gw, cudaStream_t s);
 
+// GPU activation statistics (stats.cu): ActivationStats on the device.
+struct StatsState {
+  int E = 0, W = 0;
+  long long *counts = nullptr;  // [E]
+  long long *coact = nullptr;   // [E*E]
+  uint32_t *ring = nullptr;     // [W][ceil(E/32)]
+  uint32_t *mask = nullptr;     // [ceil(E/32)] this step's set
+  long long *step = nullptr;    // steps recorded
+  int *bad = nullptr;           // INT_MAX, or the min out-of-range id of the last step
+};
+cudaError_t launch_stats_record(const StatsState &st, const int32_t *experts, long long S,
+                                cudaStream_t s);
+
 // Attention <-> MoE exchange (xfer.cu).  Ranks [0, A) own token shards,
 // ranks [A, A+M) are MoE instances g = rank - A.  One exchange region per
 // rank, identical layout everywhere.
@@ -177,6 +190,9 @@ struct janus_ctx {
   cudaStream_t cap_stream = nullptr;
   std::vector<GraphEntry> graphs;  // small LRU cache (a serving loop rotates few buffers)
   uint64_t graph_clock = 0;
+
+  // activation statistics (janus_stats_*)
+  janus::StatsState stats;
 
   // attention <-> MoE exchange
   bool xfer_ready = false;

@@ -14,7 +14,7 @@ import ctypes as C
 import numpy as np
 import torch
 
-from ._lib import OK, EUNKNOWN_EXPERT, JanusAssignment, lib
+from ._lib import EINVAL, OK, EUNKNOWN_EXPERT, JanusAssignment, lib
 from .moesim import JanusError, ReplicaMap, Scheduler, ValidationError, derive_seed
 
 
@@ -182,3 +182,55 @@ def make_inputs(T: int, k: int, d_h: int, seed: int, device) -> tuple:
     logits = torch.randn(T, k, generator=g, device=device)
     gw = torch.softmax(logits, dim=1).reshape(-1).contiguous()
     return x, gw
+
+
+class ActivationStats:
+    """Device mirror of the reference's ActivationStats (experts.hpp:18-43):
+    windowed per-expert activation counts and co-activation matrix, updated
+    from a step's routing on the GPU (janus_stats_*)."""
+
+    def __init__(self, num_experts: int, window_steps: int, device: int = 0):
+        self.device = torch.device("cuda", device)
+        self.ctx = C.c_void_p()
+        st = lib.janus_create(C.byref(self.ctx), device)
+        if st != OK:
+            raise JanusError(st, "janus_create")
+        st = lib.janus_stats_configure(self.ctx, num_experts, window_steps)
+        if st == EINVAL:
+            raise ValidationError(lib.janus_last_error(self.ctx).decode())
+        if st != OK:
+            raise JanusError(st, lib.janus_last_error(self.ctx).decode())
+        self.E, self.W = num_experts, window_steps
+
+    def record_batch(self, experts: torch.Tensor, top_k: int) -> None:
+        """record_step(activated set of this routing), asynchronously on the
+        current stream."""
+        assert experts.dtype == torch.int32 and experts.is_cuda and experts.is_contiguous()
+        st = lib.janus_stats_record_async(self.ctx, experts.data_ptr(), experts.numel() // top_k,
+                                          top_k, _cur_stream(self.device))
+        if st != OK:
+            raise JanusError(st, lib.janus_last_error(self.ctx).decode())
+
+    def check(self) -> None:
+        """Raise the reference's ValidationError if the last step was rejected."""
+        bad = C.c_int()
+        if lib.janus_stats_status(self.ctx, C.byref(bad)) == EINVAL:
+            raise ValidationError(lib.janus_last_error(self.ctx).decode())
+
+    def read(self):
+        """(counts int64 [E], coact int64 [E, E], recorded_steps)."""
+        counts = np.zeros(self.E, np.int64)
+        coact = np.zeros((self.E, self.E), np.int64)
+        rec = C.c_int()
+        st = lib.janus_stats_read(self.ctx, counts.ctypes.data_as(C.POINTER(C.c_int64)),
+                                  coact.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(rec))
+        if st != OK:
+            raise JanusError(st, lib.janus_last_error(self.ctx).decode())
+        return counts, coact, rec.value
+
+    def __del__(self):
+        try:
+            if self.ctx:
+                lib.janus_destroy(self.ctx)
+        except Exception:
+            pass

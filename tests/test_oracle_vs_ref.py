@@ -93,3 +93,22 @@ def test_latency_model_vs_ref(oracle, ref):
         routed = rng.integers(0, 5000, N).astype(np.int64)
         assert oracle.moe_layer_latency(load, routed, 4096, 1536) == \
             ref.moe_layer_latency(load, routed, 4096, 1536)
+
+
+@pytest.mark.parametrize("E,W", [(8, 1), (40, 3), (256, 6)])
+def test_activation_stats_restatement(oracle, ref, E, W):
+    """or_stats_record (the device algorithm: a ring of bitmasks) equals the
+    reference ActivationStats (experts.cpp:30-57) on random windows."""
+    rng = np.random.default_rng(E + W)
+    steps = [np.sort(rng.choice(E, int(rng.integers(0, min(E, 20) + 1)), replace=False))
+             for _ in range(4 * W + 3)]
+    st = oracle.stats_new(E, W)
+    for a in steps:
+        oracle.stats_record(st, a)
+    rc, rco = ref.stats(E, W, steps)
+    np.testing.assert_array_equal(st["counts"], rc)
+    np.testing.assert_array_equal(st["coact"], rco)
+    with pytest.raises(ValueError, match="out of range"):
+        ref.stats(E, W, [np.array([E], np.int32)])
+    with pytest.raises(ValueError, match="ascending"):
+        ref.stats(E, W, [np.array([1, 1], np.int32)])
