@@ -135,6 +135,16 @@ janus_status janus_moe_layer(janus_ctx *ctx, const void *x, const int32_t *exper
                              const float *gate_w, int num_tokens, void *out);
 
 /* ---- instrumentation ---------------------------------------------------- */
+/* host, pipelined: janus_moe_layer with the copies of neighbouring calls
+ * overlapped — H2D of call i+1 and D2H of call i-1 run on their own streams
+ * (pinned host buffers needed for overlap) while call i's layer runs.  Returns
+ * once enqueued; the caller must keep the host buffers alive and not reuse
+ * `out` / refill the inputs of a call until janus_moe_host_sync (or until two
+ * later calls were enqueued).  Errors of the scheduled batches (unknown
+ * expert) are reported by janus_moe_host_sync. */
+janus_status janus_moe_layer_host_async(janus_ctx *ctx, const void *x, const int32_t *experts,
+                                        const float *gate_w, int num_tokens, void *out);
+janus_status janus_moe_host_sync(janus_ctx *ctx);
 /* While enabled, every janus_moe_layer_async call records CUDA events on its
  * stream around the scheduler kernel (K1+K2) and around the grouped GEMMs (K4).
  * janus_profile_read synchronises, returns the summed device times (ms) and

@@ -30,6 +30,7 @@ SYMBOLS = (
     "janus_xfer_mc_create", "janus_xfer_mc_join", "janus_xfer_mc_bind", "janus_gate_async",
     "janus_moe_set_router", "janus_moe_layer_gated_async", "janus_stats_configure",
     "janus_stats_record_async", "janus_stats_read", "janus_stats_status",
+    "janus_moe_layer_host_async", "janus_moe_host_sync",
 )
 
 
@@ -90,6 +91,8 @@ def _load() -> C.CDLL:
     L.janus_stats_record_async.argtypes = [vp, vp, i64, i32, vp]
     L.janus_stats_read.argtypes = [vp, P(i64), P(i64), P(i32)]
     L.janus_stats_status.argtypes = [vp, P(i32)]
+    L.janus_moe_layer_host_async.argtypes = [vp, vp, vp, vp, i32, vp]
+    L.janus_moe_host_sync.argtypes = [vp]
     return L
 
 

@@ -137,6 +137,7 @@ janus_status janus_create(janus_ctx **out, int device) {
 }
 
 static void free_stats(janus::StatsState &st);
+static void free_host_pipe(janus_ctx *ctx);
 
 void janus_destroy(janus_ctx *ctx) {
   if (!ctx) return;
@@ -160,6 +161,7 @@ void janus_destroy(janus_ctx *ctx) {
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   janus::mc_free(ctx->xfer, ctx->device);
   free_stats(ctx->stats);
+  free_host_pipe(ctx);
   for (void *p : ctx->xfer.opened) cudaIpcCloseMemHandle(p);
   dfree(ctx->xfer.local);
   dfree(ctx->xfer.counter);
@@ -420,6 +422,7 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   dfree(ctx->ffn.y);
   dfree(ctx->ffn.tile_ctr);
   ctx->ffn.tile_ctr = nullptr;
+  free_host_pipe(ctx);  // staging sized by max_tokens
   free_assign(ctx->ws);
   dfree(ctx->ws_tile_off);
   dfree(ctx->d_x);
@@ -905,6 +908,102 @@ janus_status janus_moe_layer(janus_ctx *ctx, const void *x, const int32_t *exper
     return fail(ctx, JANUS_EUNKNOWN_EXPERT,
                 "unknown-expert: batch references expert " + std::to_string(status[1]) +
                     " with no replica in the map");
+  return JANUS_OK;
+}
+
+namespace {
+// keep the first non-OK scheduler status of the pipelined host calls
+__global__ void sticky_status_kernel(const int32_t *status, int32_t *sticky) {
+  if (status[0] != JANUS_OK && sticky[0] == JANUS_OK) {
+    sticky[0] = status[0];
+    sticky[1] = status[1];
+  }
+}
+}  // namespace
+
+static void free_host_pipe(janus_ctx *ctx) {
+  auto &hp = ctx->hp;
+  if (!hp.ready) return;
+  cudaDeviceSynchronize();
+  for (int b = 0; b < 2; ++b) {
+    dfree(hp.x[b]);
+    dfree(hp.out[b]);
+    dfree(hp.ex[b]);
+    dfree(hp.gw[b]);
+    cudaEventDestroy(hp.h2d_ev[b]);
+    cudaEventDestroy(hp.comp_ev[b]);
+    cudaEventDestroy(hp.free_ev[b]);
+  }
+  dfree(hp.sticky);
+  cudaStreamDestroy(hp.h2d);
+  cudaStreamDestroy(hp.d2h);
+  hp = janus_ctx::HostPipe{};
+}
+
+janus_status janus_moe_layer_host_async(janus_ctx *ctx, const void *x, const int32_t *experts,
+                                        const float *gate_w, int T, void *out) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (!ctx->moe_ready) return fail(ctx, JANUS_ESTATE, "moe: weights not set");
+  if (T < 0 || T > ctx->max_tokens)
+    return fail(ctx, JANUS_EINVAL, "moe: num_tokens outside [0, max_tokens]");
+  CK(cudaSetDevice(ctx->device));
+  auto &hp = ctx->hp;
+  if (!hp.ready) {
+    CK(cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking));
+    const size_t S = (size_t)ctx->max_tokens * ctx->top_k;
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaMalloc(&hp.x[b], (size_t)ctx->max_tokens * ctx->d_h * 2));
+      CK(cudaMalloc(&hp.out[b], (size_t)ctx->max_tokens * ctx->d_h * 2));
+      CK(dalloc(&hp.ex[b], S));
+      CK(dalloc(&hp.gw[b], S));
+      CK(cudaEventCreateWithFlags(&hp.h2d_ev[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&hp.comp_ev[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&hp.free_ev[b], cudaEventDisableTiming));
+    }
+    CK(dalloc(&hp.sticky, 2));
+    CK(cudaMemset(hp.sticky, 0, 2 * sizeof(int32_t)));
+    hp.ready = true;
+  }
+  const int b = (int)(hp.calls & 1);
+  const size_t S = (size_t)T * ctx->top_k;
+  // H2D into set b once call i-2 (same set) has been copied out
+  CK(cudaStreamWaitEvent(hp.h2d, hp.free_ev[b], 0));
+  CK(cudaMemcpyAsync(hp.x[b], x, (size_t)T * ctx->d_h * 2, cudaMemcpyHostToDevice, hp.h2d));
+  CK(cudaMemcpyAsync(hp.ex[b], experts, S * 4, cudaMemcpyHostToDevice, hp.h2d));
+  CK(cudaMemcpyAsync(hp.gw[b], gate_w, S * 4, cudaMemcpyHostToDevice, hp.h2d));
+  CK(cudaEventRecord(hp.h2d_ev[b], hp.h2d));
+  CK(cudaStreamWaitEvent(ctx->stream, hp.h2d_ev[b], 0));
+  st = janus_moe_layer_async(ctx, hp.x[b], hp.ex[b], hp.gw[b], T, hp.out[b], nullptr, ctx->stream);
+  if (st != JANUS_OK) return st;
+  sticky_status_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ws.status, hp.sticky);
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  CK(cudaEventRecord(hp.comp_ev[b], ctx->stream));
+  CK(cudaStreamWaitEvent(hp.d2h, hp.comp_ev[b], 0));
+  CK(cudaMemcpyAsync(out, hp.out[b], (size_t)T * ctx->d_h * 2, cudaMemcpyDeviceToHost, hp.d2h));
+  CK(cudaEventRecord(hp.free_ev[b], hp.d2h));
+  hp.calls++;
+  return JANUS_OK;
+}
+
+janus_status janus_moe_host_sync(janus_ctx *ctx) {
+  if (!ctx) return JANUS_EINVAL;
+  auto &hp = ctx->hp;
+  if (!hp.ready) return JANUS_OK;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(hp.h2d));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(hp.d2h));
+  int32_t sticky[2];
+  CK(cudaMemcpy(sticky, hp.sticky, sizeof(sticky), cudaMemcpyDeviceToHost));
+  if (sticky[0] != JANUS_OK) {
+    CK(cudaMemset(hp.sticky, 0, sizeof(sticky)));
+    return fail(ctx, JANUS_EUNKNOWN_EXPERT,
+                "unknown-expert: batch references expert " + std::to_string(sticky[1]) +
+                    " with no replica in the map");
+  }
   return JANUS_OK;
 }
 

@@ -132,6 +132,24 @@ class MoELayer:
             raise JanusError(st, self.sched.last_error())
         return out
 
+    def forward_host_async(self, x: torch.Tensor, experts: torch.Tensor, gate_w: torch.Tensor,
+                           out: torch.Tensor) -> None:
+        """Pipelined host call (janus_moe_layer_host_async): enqueue H2D, the
+        layer and D2H; the copies of neighbouring calls overlap the layer.
+        Call :meth:`host_sync` before reading ``out``."""
+        T = x.shape[0]
+        st = lib.janus_moe_layer_host_async(self.ctx, x.data_ptr(), experts.data_ptr(),
+                                            gate_w.data_ptr(), T, out.data_ptr())
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+
+    def host_sync(self) -> None:
+        st = lib.janus_moe_host_sync(self.ctx)
+        if st == EUNKNOWN_EXPERT:
+            raise ValidationError(self.sched.last_error())
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+
     def launches(self) -> int:
         return self.sched.launches()
 

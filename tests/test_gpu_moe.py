@@ -206,3 +206,36 @@ def test_empty_step(J):
                         torch.zeros(0, dtype=torch.float32, device="cuda"))
     torch.cuda.synchronize()
     assert out.shape == (0, 256)
+
+
+def test_pipelined_host_api_matches_device_path(J):
+    """janus_moe_layer_host_async: several calls in flight (two staging sets,
+    copies overlapped with the layer) give the device path's bytes; an unknown
+    expert in any call is reported at janus_moe_host_sync."""
+    import torch
+    rm = J.config_map("c2")
+    T, k = 200, 8
+    layer = make_layer(J, rm, 2048, 768, T, k)
+    from paper_2512_13525_b200.moe import make_inputs
+    calls = []
+    for i in range(5):
+        b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, k, 0x30, i)
+        x, gw = make_inputs(T, k, 2048, i, "cuda")
+        ex = torch.from_numpy(b.experts).cuda()
+        ref = layer.forward(x, ex, gw).cpu()
+        calls.append((x.cpu().pin_memory(), ex.cpu().pin_memory(), gw.cpu().pin_memory(),
+                      torch.empty(T, 2048, dtype=torch.bfloat16).pin_memory(), ref))
+    torch.cuda.synchronize()
+    for xh, eh, gh, oh, _ in calls:
+        layer.forward_host_async(xh, eh, gh, oh)
+    layer.host_sync()
+    for _, _, _, oh, ref in calls:
+        assert torch.equal(oh, ref)
+    bad = calls[2][1].clone()
+    bad[3] = 1000
+    layer.forward_host_async(calls[0][0], calls[0][1], calls[0][2], calls[0][3])
+    layer.forward_host_async(calls[1][0], bad.pin_memory(), calls[1][2], calls[1][3])
+    layer.forward_host_async(calls[2][0], calls[2][1], calls[2][2], calls[2][3])
+    with pytest.raises(J.ValidationError, match="unknown-expert: batch references expert 1000"):
+        layer.host_sync()
+    layer.host_sync()  # the error was consumed
