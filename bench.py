@@ -513,25 +513,46 @@ def run_box(args):
     t0 = time.perf_counter()
     e0_ = epoch[0]
     if role == "attention":
-        # per step: H2D of step i+1's shard, dispatch i+1, combine i, D2H of i
+        # per step: H2D of step i+1's shard (copy stream), dispatch i+1,
+        # combine i (compute stream), D2H of step i's output (second copy
+        # stream) — every step's bytes cross PCIe, overlapped with the layer
         xd2 = [xd, torch.empty_like(xd)]
         exd2 = [exd, torch.empty_like(exd)]
         gwd2 = [gwd, torch.empty_like(gwd)]
+        out2 = [out, torch.empty_like(out)]
+        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]    # inputs of slot b landed
+        ev_used = [torch.cuda.Event(), torch.cuda.Event()]  # dispatch read slot b
+        ev_out = [torch.cuda.Event(), torch.cuda.Event()]   # combine wrote out[b]
+        ev_read = [torch.cuda.Event(), torch.cuda.Event()]  # D2H read out[b]
 
         def h2d_dispatch(i):
             b = i & 1
-            xd2[b].copy_(xh, non_blocking=True)
-            exd2[b].copy_(exh[i % N_BATCHES], non_blocking=True)
-            gwd2[b].copy_(gwh, non_blocking=True)
+            with torch.cuda.stream(h2d_s):
+                if i >= 2:
+                    h2d_s.wait_event(ev_used[b])
+                xd2[b].copy_(xh, non_blocking=True)
+                exd2[b].copy_(exh[i % N_BATCHES], non_blocking=True)
+                gwd2[b].copy_(gwh, non_blocking=True)
+                ev_in[b].record(h2d_s)
+            s.wait_event(ev_in[b])
             box.dispatch(xd2[b], exd2[b], gwd2[b], T, e0_ + i + 1, stream)
+            ev_used[b].record(s)
 
         h2d_dispatch(0)
         for i in range(args.steps):
             if i + 1 < args.steps:
                 h2d_dispatch(i + 1)
-            box.combine(out, T, e0_ + i + 1, stream)
-            oh.copy_(out, non_blocking=True)
-            torch.cuda.synchronize()
+            b = i & 1
+            if i >= 2:
+                s.wait_event(ev_read[b])
+            box.combine(out2[b], T, e0_ + i + 1, stream)
+            ev_out[b].record(s)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(ev_out[b])
+                oh.copy_(out2[b], non_blocking=True)
+                ev_read[b].record(d2h_s)
+        torch.cuda.synchronize()
     else:
         for i in range(args.steps):
             box.moe_step(T, e0_ + i + 1, stream)
