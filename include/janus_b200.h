@@ -139,8 +139,7 @@ janus_status janus_moe_layer(janus_ctx *ctx, const void *x, const int32_t *exper
  * overlapped — H2D of call i+1 and D2H of call i-1 run on their own streams
  * (pinned host buffers needed for overlap) while call i's layer runs.  Returns
  * once enqueued; the caller must keep the host buffers alive and not reuse
- * `out` / refill the inputs of a call until janus_moe_host_sync (or until two
- * later calls were enqueued).  Errors of the scheduled batches (unknown
+ * `out` / refill the inputs of a call until janus_moe_host_sync.  Errors of the scheduled batches (unknown
  * expert) are reported by janus_moe_host_sync. */
 janus_status janus_moe_layer_host_async(janus_ctx *ctx, const void *x, const int32_t *experts,
                                         const float *gate_w, int num_tokens, void *out);

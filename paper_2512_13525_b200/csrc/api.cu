@@ -925,7 +925,7 @@ static void free_host_pipe(janus_ctx *ctx) {
   auto &hp = ctx->hp;
   if (!hp.ready) return;
   cudaDeviceSynchronize();
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < janus_ctx::kHostSets; ++b) {
     dfree(hp.x[b]);
     dfree(hp.out[b]);
     dfree(hp.ex[b]);
@@ -953,7 +953,7 @@ janus_status janus_moe_layer_host_async(janus_ctx *ctx, const void *x, const int
     CK(cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking));
     const size_t S = (size_t)ctx->max_tokens * ctx->top_k;
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < janus_ctx::kHostSets; ++b) {
       CK(cudaMalloc(&hp.x[b], (size_t)ctx->max_tokens * ctx->d_h * 2));
       CK(cudaMalloc(&hp.out[b], (size_t)ctx->max_tokens * ctx->d_h * 2));
       CK(dalloc(&hp.ex[b], S));
@@ -966,9 +966,9 @@ janus_status janus_moe_layer_host_async(janus_ctx *ctx, const void *x, const int
     CK(cudaMemset(hp.sticky, 0, 2 * sizeof(int32_t)));
     hp.ready = true;
   }
-  const int b = (int)(hp.calls & 1);
+  const int b = (int)(hp.calls % janus_ctx::kHostSets);
   const size_t S = (size_t)T * ctx->top_k;
-  // H2D into set b once call i-2 (same set) has been copied out
+  // H2D into set b once the call that last used it has been copied out
   CK(cudaStreamWaitEvent(hp.h2d, hp.free_ev[b], 0));
   CK(cudaMemcpyAsync(hp.x[b], x, (size_t)T * ctx->d_h * 2, cudaMemcpyHostToDevice, hp.h2d));
   CK(cudaMemcpyAsync(hp.ex[b], experts, S * 4, cudaMemcpyHostToDevice, hp.h2d));

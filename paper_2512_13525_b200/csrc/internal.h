@@ -191,16 +191,18 @@ struct janus_ctx {
   std::vector<GraphEntry> graphs;  // small LRU cache (a serving loop rotates few buffers)
   uint64_t graph_clock = 0;
 
-  // pipelined host API (janus_moe_layer_host_async): two device staging sets;
-  // H2D on one stream, the layer on `stream`, D2H on a third, so the copies of
-  // neighbouring calls overlap the layer
+  // pipelined host API (janus_moe_layer_host_async): kHostSets device staging
+  // sets; H2D on one stream, the layer on `stream`, D2H on a third, so the
+  // copies of neighbouring calls overlap the layer.  A set is busy from its
+  // H2D to its D2H (~H2D + layer + D2H), so three sets keep the layer fed.
+  static constexpr int kHostSets = 3;
   struct HostPipe {
     bool ready = false;
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t h2d_ev[2] = {}, comp_ev[2] = {}, free_ev[2] = {};
-    void *x[2] = {}, *out[2] = {};
-    int32_t *ex[2] = {};
-    float *gw[2] = {};
+    cudaEvent_t h2d_ev[kHostSets] = {}, comp_ev[kHostSets] = {}, free_ev[kHostSets] = {};
+    void *x[kHostSets] = {}, *out[kHostSets] = {};
+    int32_t *ex[kHostSets] = {};
+    float *gw[kHostSets] = {};
     int32_t *sticky = nullptr;  // first failing call's scheduler status (device)
     uint64_t calls = 0;
   } hp;
