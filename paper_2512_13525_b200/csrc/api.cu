@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 using janus::DevMap;
 
@@ -523,6 +524,7 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     ctx->prof_calls++;
     CK(cudaEventRecord(ev[0], s));
   }
+  janus::sm100::pdl_enabled = ev == nullptr;  // events between PDL kernels would mis-time them
   st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, ctx->ws_tile_off, s);
   if (st != JANUS_OK) return st;
   if (ev) CK(cudaEventRecord(ev[1], s));
