@@ -127,6 +127,11 @@ janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *d_w
  * With a single-instance weight store (instance >= 0) out receives this
  * instance's partial sum (tokens routed elsewhere contribute 0).
  * If `assign` is non-NULL the scheduling outputs are also written there. */
+/* DeepSeek-V3-style shared expert (one expert on every
+ * token, weight 1, added after the routed slots): w13 [2*d_e][d_h] = [Wg; Wu],
+ * w2 [d_h][d_e], bf16, caller-owned; NULL disables.  Computed by the
+ * single-GPU layer, and by MoE instance 0 of a box (NVLS transport). */
+janus_status janus_moe_set_shared(janus_ctx *ctx, const void *d_w13, const void *d_w2);
 janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                                    const float *d_gate_w, int num_tokens, void *d_out,
                                    const janus_assignment *assign, void *stream);

@@ -30,7 +30,7 @@ SYMBOLS = (
     "janus_xfer_mc_create", "janus_xfer_mc_join", "janus_xfer_mc_bind", "janus_gate_async",
     "janus_moe_set_router", "janus_moe_layer_gated_async", "janus_stats_configure",
     "janus_stats_record_async", "janus_stats_read", "janus_stats_status",
-    "janus_moe_layer_host_async", "janus_moe_host_sync",
+    "janus_moe_layer_host_async", "janus_moe_host_sync", "janus_moe_set_shared",
 )
 
 
@@ -93,6 +93,7 @@ def _load() -> C.CDLL:
     L.janus_stats_status.argtypes = [vp, P(i32)]
     L.janus_moe_layer_host_async.argtypes = [vp, vp, vp, vp, i32, vp]
     L.janus_moe_host_sync.argtypes = [vp]
+    L.janus_moe_set_shared.argtypes = [vp, vp, vp]
     return L
 
 

@@ -139,6 +139,7 @@ janus_status janus_create(janus_ctx **out, int device) {
 
 static void free_stats(janus::StatsState &st);
 static void free_host_pipe(janus_ctx *ctx);
+static void free_shared(janus_ctx *ctx);
 
 void janus_destroy(janus_ctx *ctx) {
   if (!ctx) return;
@@ -163,6 +164,7 @@ void janus_destroy(janus_ctx *ctx) {
   janus::mc_free(ctx->xfer, ctx->device);
   free_stats(ctx->stats);
   free_host_pipe(ctx);
+  free_shared(ctx);
   for (void *p : ctx->xfer.opened) cudaIpcCloseMemHandle(p);
   dfree(ctx->xfer.local);
   dfree(ctx->xfer.counter);
@@ -271,7 +273,8 @@ janus_status janus_replica_order(const janus_ctx *ctx, int32_t *qidx, int32_t *q
 
 static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T, int k,
                                  int policy, uint64_t seed, const janus_assignment &out,
-                                 int32_t *tile_off, cudaStream_t stream) {
+                                 int32_t *tile_off, cudaStream_t stream,
+                                 int32_t *shared_off = nullptr, int shared_tile_n = 0) {
   if (T < 0 || k <= 0 || (int64_t)T * k > (int64_t)1 << 30)
     return fail(ctx, JANUS_EINVAL, "batch: num_tokens must be >= 0 and top_k >= 1");
   if (policy != JANUS_POLICY_AEBS && policy != JANUS_POLICY_RANDOM)
@@ -294,6 +297,8 @@ static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T
   // its last tile (one pass over the weights); in the tensor regime the wide
   // tile's halved weight prefetch depth costs more than it saves (measured)
   a.merge_tail = a.tile_n <= 64;
+  a.shared_off = shared_off;
+  a.shared_tile_n = shared_tile_n;
   cudaError_t e = janus::launch_schedule(a, stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aebs_schedule_kernel");
   ctx->launches += 1;
@@ -424,6 +429,7 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   dfree(ctx->ffn.tile_ctr);
   ctx->ffn.tile_ctr = nullptr;
   free_host_pipe(ctx);  // staging sized by max_tokens
+  free_shared(ctx);
   free_assign(ctx->ws);
   dfree(ctx->ws_tile_off);
   dfree(ctx->d_x);
@@ -458,6 +464,52 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   ctx->ffn.S_alloc = S_alloc;
   ctx->moe_ready = false;
   clear_graphs(ctx);
+  return JANUS_OK;
+}
+
+static void free_shared(janus_ctx *ctx) {
+  janus::FfnPlan &ps = ctx->ffn_shared;
+  dfree(ps.xp);
+  dfree(ps.h);
+  dfree(ps.y);
+  dfree(ps.tile_ctr);
+  dfree(ctx->shared_off);
+  ctx->shared_off = nullptr;
+  ps = janus::FfnPlan{};
+  ctx->shared = false;
+}
+
+janus_status janus_moe_set_shared(janus_ctx *ctx, const void *w13, const void *w2) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (!ctx->ffn.h) return fail(ctx, JANUS_ESTATE, "moe: janus_moe_configure first");
+  CK(cudaSetDevice(ctx->device));
+  clear_graphs(ctx);
+  if (!w13 || !w2) {  // disable
+    free_shared(ctx);
+    return JANUS_OK;
+  }
+  janus::FfnPlan &ps = ctx->ffn_shared;
+  if (!ps.xp) {
+    const int rows = ctx->max_tokens + janus::kTileN;  // tail room for the last token box
+    ps.d_h = ctx->d_h;
+    ps.d_e = ctx->d_e;
+    ps.S_alloc = rows;
+    CK(cudaMalloc(&ps.xp, (size_t)rows * ps.d_h * 2));
+    CK(cudaMalloc(&ps.h, (size_t)rows * ps.d_e * 2));
+    CK(cudaMalloc(&ps.y, (size_t)rows * ps.d_h * 2));
+    CK(cudaMemset(ps.xp, 0, (size_t)rows * ps.d_h * 2));
+    CK(cudaMemset(ps.h, 0, (size_t)rows * ps.d_e * 2));
+    CK(dalloc(&ps.tile_ctr, 4));
+    CK(cudaMemset(ps.tile_ctr, 0, 4 * sizeof(unsigned)));
+    CK(dalloc(&ctx->shared_off, 4));
+  }
+  ps.q_begin = 0;
+  ps.q_end = 1;
+  ps.w13 = w13;
+  ps.w2 = w2;
+  CK(janus::build_ffn_tensor_maps(ps));
+  ctx->shared = true;
   return JANUS_OK;
 }
 
@@ -525,16 +577,24 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     CK(cudaEventRecord(ev[0], s));
   }
   janus::sm100::pdl_enabled = ev == nullptr;  // events between PDL kernels would mis-time them
-  st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, ctx->ws_tile_off, s);
+  // the shared expert (every token) runs on the single-GPU layer, and on MoE
+  // instance 0 of a box (its partial sums carry it)
+  const bool shared = ctx->shared && ctx->instance <= 0;
+  janus::FfnPlan &ps = ctx->ffn_shared;
+  if (shared) ps.tile_n = T <= 64 ? 64 : janus::kTileN;
+  st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, ctx->ws_tile_off, s,
+                    shared ? ctx->shared_off : nullptr, shared ? ps.tile_n : 0);
   if (st != JANUS_OK) return st;
   if (ev) CK(cudaEventRecord(ev[1], s));
   janus::FfnPlan &p = ctx->ffn;
-  cudaError_t e =
-      janus::launch_permute(d_x, a.slot_row, a.instance, ctx->instance, T * k, k, p.d_h, p.xp, s);
+  cudaError_t e = janus::launch_permute(d_x, a.slot_row, a.instance, ctx->instance, T * k, k,
+                                        p.d_h, p.xp, shared ? ps.xp : nullptr, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "permute_kernel");
   int launches = 0;
   if (ev) CK(cudaEventRecord(ev[2], s));
   e = janus::launch_ffn(p, a.group_off, ctx->ws_tile_off, s, &launches);
+  if (e == cudaSuccess && shared)
+    e = janus::launch_ffn(ps, ctx->shared_off, ctx->shared_off + 2, s, &launches);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "grouped_gemm_kernel");
   if (ev) CK(cudaEventRecord(ev[3], s));
   if (push_epoch && ctx->xfer.mc) {
@@ -544,15 +604,16 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
                               reinterpret_cast<void *>(x.uc_va + x.mpart_off +
                                                        janus::xfer_slot(push_epoch) * x.mslot),
-                              s);
+                              s, shared ? ps.y : nullptr);
     if (e == cudaSuccess) e = janus::launch_signal_combine(x, push_epoch, s);
     launches += 1;
-  } else if (push_epoch)
+  } else if (push_epoch) {
+    if (shared) return fail(ctx, JANUS_EUNSUPPORTED, "moe: shared expert needs the NVLS transport");
     e = janus::launch_combine_push(ctx->xfer, p.y, a.slot_row, a.instance, d_gate_w, T,
                                    push_epoch, s);
-  else
+  } else
     e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
-                              d_out, s);
+                              d_out, s, shared ? ps.y : nullptr);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
   ctx->launches += 2 + launches;  // permute, combine, GEMMs (launch_sched counts itself)
   return JANUS_OK;

@@ -35,7 +35,7 @@ constexpr int kWarpsPerBlock = 4;
 
 __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__restrict__ slot_row,
                                const int32_t *__restrict__ slot_inst, int instance, int T, int k,
-                               int vec, uint4 *__restrict__ xp) {
+                               int vec, uint4 *__restrict__ xp, uint4 *__restrict__ xp_shared) {
   sm100::pdl_trigger();
   sm100::pdl_wait();  // slot_row / slot_inst from K1
   const int lane = threadIdx.x & 31;
@@ -46,6 +46,17 @@ __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__res
   const uint4 *src = x + (size_t)t * vec;
   uint4 v[kPermU];
   bool loaded = false;  // x is read only if some slot of t is routed here
+  if (xp_shared) {      // the shared expert takes every token, in token order
+#pragma unroll
+    for (int u = 0; u < kPermU; ++u) {
+      const int c = c0 + 32 * u;
+      if (c < vec) {
+        v[u] = __ldg(src + c);
+        xp_shared[(size_t)t * vec + c] = v[u];
+      }
+    }
+    loaded = true;
+  }
   for (int j0 = 0; j0 < k; j0 += 32) {
     const int j = j0 + lane;
     int row = -1;
@@ -87,7 +98,8 @@ template <int G>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
     combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
                    const int32_t *__restrict__ slot_inst, int instance,
-                   const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out) {
+                   const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out,
+                   const uint4 *__restrict__ y_shared) {
   sm100::pdl_trigger();
   sm100::pdl_wait();  // y from the down GEMM
   const int lane = threadIdx.x & 31;
@@ -156,6 +168,21 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
         }
     }
   }
+  if (y_shared) {  // the shared expert, weight 1, after the routed slots
+#pragma unroll
+    for (int u = 0; u < kCombU; ++u) {
+      const int c = c0 + 32 * u;
+      if (c >= vec) continue;
+      const uint4 v = __ldg(y_shared + (size_t)t * vec + c);
+      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        acc[u][2 * e] += f.x;
+        acc[u][2 * e + 1] += f.y;
+      }
+    }
+  }
 #pragma unroll
   for (int u = 0; u < kCombU; ++u) {
     const int c = c0 + 32 * u;
@@ -171,26 +198,29 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
 }  // namespace
 
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
-                           int instance, int S, int k, int d_h, void *xp, cudaStream_t s) {
+                           int instance, int S, int k, int d_h, void *xp, void *xp_shared,
+                           cudaStream_t s) {
   if (S == 0) return cudaSuccess;
   const int T = S / k, vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kPermU - 1) / (32 * kPermU));
   const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
   return sm100::launch_pdl(permute_kernel, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
                            reinterpret_cast<const uint4 *>(x), slot_row, slot_instance, instance,
-                           T, k, vec, reinterpret_cast<uint4 *>(xp));
+                           T, k, vec, reinterpret_cast<uint4 *>(xp),
+                           reinterpret_cast<uint4 *>(xp_shared));
 }
 
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
-                           cudaStream_t s) {
+                           cudaStream_t s, const void *y_shared) {
   if (T == 0) return cudaSuccess;
   const int vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kCombU - 1) / (32 * kCombU));
   const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
   return sm100::launch_pdl(combine_kernel<4>, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
                            reinterpret_cast<const uint4 *>(y), slot_row, slot_instance, instance,
-                           gate_w, T, k, vec, reinterpret_cast<uint4 *>(out));
+                           gate_w, T, k, vec, reinterpret_cast<uint4 *>(out),
+                           reinterpret_cast<const uint4 *>(y_shared));
 }
 
 }  // namespace janus

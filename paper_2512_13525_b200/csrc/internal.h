@@ -33,6 +33,8 @@ struct SchedArgs {
   uint64_t *trace;     // [7] phase timestamps (%globaltimer), optional
   int id_bits;         // bits of the largest expert id (ballot-based peer matching)
   int merge_tail;      // 1: a group's last n-tile also takes the remainder (wide tiles)
+  int32_t *shared_off;  // optional [4]: the shared expert's {0, T} rows and {0, n-tiles}
+  int shared_tile_n;
 };
 
 inline int id_bits_for(int E) {
@@ -62,14 +64,18 @@ struct FfnPlan {
 };
 
 cudaError_t build_ffn_tensor_maps(FfnPlan &p);
+// xp_shared (optional): also store row t of x at xp_shared[t] (the shared
+// expert's token rows, in token order)
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
-                           int instance, int S, int k, int d_h, void *xp, cudaStream_t s);
+                           int instance, int S, int k, int d_h, void *xp, void *xp_shared,
+                           cudaStream_t s);
 // gate/up GEMM with fused SwiGLU, then the down GEMM; 2 launches.
 cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
                        cudaStream_t s, int *launches);
+// y_shared (optional): + y_shared[t] (weight 1) after the k routed slots
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
-                           cudaStream_t s);
+                           cudaStream_t s, const void *y_shared = nullptr);
 
 // MoE-side gating (gate.cu): router GEMM + top-k + softmax of the top-k logits.
 bool gate_shape_ok(int d_h, int E, int k);
@@ -164,6 +170,11 @@ struct janus_ctx {
   bool moe_ready = false;
   int d_h = 0, d_e = 0, max_tokens = 0, top_k = 0, instance = -1;
   janus::FfnPlan ffn;
+  // DeepSeek-V3-style shared expert (janus_moe_set_shared): a dense SwiGLU over
+  // every token, its own GEMM plan over token-ordered rows that K3 also writes
+  bool shared = false;
+  janus::FfnPlan ffn_shared;
+  int32_t *shared_off = nullptr;  // [4] {0, T} rows, {0, n-tiles}
   janus_assignment ws{};      // device workspace for the layer's assignment
   int32_t *ws_tile_off = nullptr;
   // staging for the host MoE API

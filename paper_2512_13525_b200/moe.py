@@ -132,6 +132,21 @@ class MoELayer:
             raise JanusError(st, self.sched.last_error())
         return out
 
+    def set_shared(self, w13: torch.Tensor | None, w2: torch.Tensor | None = None) -> None:
+        """DeepSeek-V3-style shared expert on every token (weight 1):
+        w13 [2*d_e][d_h] = [Wg; Wu], w2 [d_h][d_e] bf16; None disables."""
+        if w13 is None:
+            self.shared_w = None
+            st = lib.janus_moe_set_shared(self.ctx, None, None)
+        else:
+            assert w13.shape == (2 * self.d_e, self.d_h) and w2.shape == (self.d_h, self.d_e)
+            assert w13.dtype == w2.dtype == torch.bfloat16 and w13.is_contiguous()
+            assert w2.is_contiguous() and w13.is_cuda and w2.is_cuda
+            self.shared_w = (w13, w2)  # keep alive: the context stores raw pointers
+            st = lib.janus_moe_set_shared(self.ctx, w13.data_ptr(), w2.data_ptr())
+        if st != OK:
+            raise JanusError(st, self.sched.last_error())
+
     def forward_host_async(self, x: torch.Tensor, experts: torch.Tensor, gate_w: torch.Tensor,
                            out: torch.Tensor) -> None:
         """Pipelined host call (janus_moe_layer_host_async): enqueue H2D, the

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls"])
+    ap.add_argument("--shared", action="store_true", help="add a shared expert (NVLS only)")
     ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
                     help="2: dispatch step s+1 before combining step s (double-buffered slots)")
     args = ap.parse_args()
@@ -50,11 +51,19 @@ def main():
     if plan.role(rank) == "moe":
         layer = MoELayer(rmap, d_h, d_e, T, k, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
+    if args.shared:
+        from paper_2512_13525_b200.moe import expert_weights
+        wg, wu, wd = expert_weights(99, d_h, d_e, 5, dev)
+        shared_w = (torch.cat([wg, wu]).contiguous(), wd.contiguous())
+        if layer is not None:
+            layer.set_shared(*shared_w)
     box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local, transport=args.transport)
     full = None
     if plan.role(rank) == "attention":
         full = MoELayer(rmap, d_h, d_e, T, k, instance=-1, device=local)
         full.set_weights(*build_weight_store(full, seed=1))
+        if args.shared:
+            full.set_shared(*shared_w)
 
     stream = torch.cuda.current_stream(dev).cuda_stream
     result = {"rank": rank, "role": plan.role(rank), "steps": [], "transport": box.transport}
@@ -110,7 +119,7 @@ def main():
         torch.cuda.synchronize()
     result["timed_out"] = box.timed_out()
     os.makedirs(args.out, exist_ok=True)
-    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}_rank{rank}.json"), "w") as f:
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}_rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
     dist.destroy_process_group()

@@ -40,3 +40,25 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
         if r["role"] == "attention":
             for s in r["steps"]:
                 assert s["bad"] == 0, s
+
+
+def test_box_exchange_with_shared_expert():
+    """The shared expert in a box: MoE instance 0 adds it to its partials
+    (NVLS transport, two steps in flight)."""
+    attn, moe = 1, 3
+    if gpus() < attn + moe:
+        pytest.skip(f"needs {attn + moe} GPUs (one rank per GPU)")
+    out = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={attn + moe}", "--master-addr", "127.0.0.1", "--master-port",
+           "29777", os.path.join(ROOT, "tests", "dist_worker.py"), "--attn", str(attn), "--moe",
+           str(moe), "--out", out, "--transport", "nvls", "--inflight", "2", "--shared"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
+    assert len(res) == attn + moe
+    for r in res:
+        assert not r["timed_out"], r
+        if r["role"] == "attention":
+            for s_ in r["steps"]:
+                assert s_["bad"] == 0, s_

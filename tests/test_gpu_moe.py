@@ -239,3 +239,43 @@ def test_pipelined_host_api_matches_device_path(J):
     with pytest.raises(J.ValidationError, match="unknown-expert: batch references expert 1000"):
         layer.host_sync()
     layer.host_sync()  # the error was consumed
+
+
+@pytest.mark.parametrize("T", [3, 64, 300])
+def test_shared_expert(J, oracle, T):
+    """DS-V3-style shared expert (A13): out = Σ_j w·y_e(x) + y_shared(x)."""
+    import torch
+    from paper_2512_13525_b200.moe import expert_weights
+    rm = J.ReplicaMap.from_hosts(1, 16, [[0]] * 16)
+    layer = make_layer(J, rm, 256, 128, 300, 4)
+    wg, wu, wd = expert_weights(999, 256, 128, 7, "cuda")
+    layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
+    b = J.gen_batch(J.RoutingPattern.zipf(16, 1.0), T, 4, 3, T)
+    x, ex, gw, out = run(J, layer, b.experts, T)
+    ref = oracle_layer_out(oracle, layer, x, ex, gw)
+    ref += oracle.expert_swiglu(u16(x), u16(wg), u16(wu), u16(wd), round_h=True, nthreads=8)
+    check_close(bf16_to_f32(u16(out)), ref, f"shared T={T}")
+    layer.set_shared(None)  # back to routed experts only
+    x, ex, gw, out = run(J, layer, b.experts, T)
+    check_close(bf16_to_f32(u16(out)), oracle_layer_out(oracle, layer, x, ex, gw), "unshared")
+
+
+def test_deepseek_v3_shape_with_shared_expert_sampled_tokens(J, oracle):
+    """c4 expert shape (DS-V3: d_h 7168, d_e 2048, top-8, + 1 shared expert) on
+    24 of its routed experts (the weight store of all 256 would be 22 GB of
+    oracle reads); checks the wide-row paths (K = 7168: 112 k-blocks, 14 KB
+    rows in K3/K5) and the shared expert at that shape."""
+    import torch
+    from paper_2512_13525_b200.moe import expert_weights
+    E, d_h, d_e, k, T = 24, 7168, 2048, 8, 200
+    rm = J.ReplicaMap.from_hosts(1, E, [[0]] * E)
+    layer = make_layer(J, rm, d_h, d_e, T, k)
+    wg, wu, wd = expert_weights(256, d_h, d_e, 7, "cuda")
+    layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
+    b = J.gen_batch(J.RoutingPattern.zipf(E, 1.0), T, k, 0xD5, T)
+    x, ex, gw, out = run(J, layer, b.experts, T)
+    tokens = np.random.default_rng(1).choice(T, 12, replace=False)
+    ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens)
+    xs = u16(x)[tokens]
+    ref += oracle.expert_swiglu(xs, u16(wg), u16(wu), u16(wd), round_h=True, nthreads=8)
+    check_close(bf16_to_f32(u16(out))[tokens], ref, "DS-V3 shape + shared")
