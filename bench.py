@@ -37,7 +37,44 @@ sys.path.insert(0, ROOT)
 E, K_TOP, D_H, D_E = 128, 8, 2048, 768
 SEED = 0x30
 MAP = "c2"
+SHARED = False
+SHAPE_NAME = "c2: Qwen3-30B-A3B-shaped MoE layer (128 experts, top-8, d_h=2048, d_e=768, SwiGLU)"
 N_BATCHES = 8  # distinct routing batches rotated through the timed steps
+
+# --shape: the BASELINE configs' expert shapes (the default c2 is the headline;
+# the others are reported in profiles/, not the driver's scaling line)
+SHAPES = {
+    "c2": (128, 8, 2048, 768, 0x30, "c2", False, SHAPE_NAME),
+    "c3": (128, 8, 4096, 1536, 0x235, "c3", False,
+           "c3: Qwen3-235B-A22B-shaped MoE layer (128 experts, top-8, d_h=4096, d_e=1536)"),
+    "c4": (256, 8, 7168, 2048, 0xD5, "c4", True,
+           "c4: DeepSeek-V3-shaped MoE layer (256 routed experts + 1 shared, top-8, d_h=7168, "
+           "d_e=2048)"),
+}
+
+
+def apply_shape(name):
+    global E, K_TOP, D_H, D_E, SEED, MAP, SHARED, SHAPE_NAME
+    E, K_TOP, D_H, D_E, SEED, MAP, SHARED, SHAPE_NAME = SHAPES[name]
+
+
+def shape_map(J, M):
+    """Replica map for M MoE instances of the current shape."""
+    if MAP == "c2":
+        return J.config_map("c2" if M == 1 else f"c2_m{M}"), f"c2{'' if M == 1 else f'_m{M}'}"
+    if MAP == "c3":
+        return J.config_map(f"c3_m{M}"), f"c3_m{M}"
+    if M == 1:  # c4 on one GPU: every expert local
+        return J.ReplicaMap.from_hosts(1, E, [[0]] * E), "one replica per expert"
+    return J.config_map(f"c4_n{M}"), f"c4_n{M}"
+
+
+def set_shared_expert(layer, dev):
+    if SHARED and layer.instance <= 0:
+        import torch
+        from paper_2512_13525_b200.moe import expert_weights
+        wg, wu, wd = expert_weights(E, D_H, D_E, 1, dev)
+        layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
 
 
 def peaks():
@@ -109,7 +146,7 @@ def cpu_sample(T, tokens_sample, batches, layer_experts_w, nthreads):
 
     import paper_2512_13525_b200 as J
     ref, orc = Ref(), Oracle()
-    rm = J.config_map(MAP)
+    rm, _ = shape_map(J, 1)
     m = CSRMap(rm.num_experts, rm.num_instances, rm.slots_per_instance, *rm.csr())
     b0 = batches[0]
     t_sched = ref.time_schedule(np.concatenate(batches), T, K_TOP, m, "schedule", reps=21) * 1e-6
@@ -196,13 +233,19 @@ def run_reference(args):
 
 
 def workload_config(T, args):
-    return {"workload": "c2: Qwen3-30B-A3B-shaped MoE layer (128 experts, top-8, d_h=2048, "
-                        "d_e=768, SwiGLU) on 1 B200 per rank: AEBS scheduler + grouped FFN",
+    wbytes = E * 3 * D_H * D_E * 2 + (3 * D_H * D_E * 2 if SHARED else 0)
+    return {"workload": SHAPE_NAME + " on 1 B200 per rank: AEBS scheduler + grouped FFN",
             "tokens_per_step": T, "experts": E, "top_k": K_TOP, "d_hidden": D_H,
-            "d_expert": D_E, "routing": "Zipf s=1.0 via gen_batch, seed 0x30",
-            "replica_map": "maps/c2.map (reference placement pipeline)",
-            "l2": "inputs > L2: 1.21 GB expert weights streamed from HBM every step",
+            "d_expert": D_E, "shared_expert": SHARED,
+            "routing": f"Zipf s=1.0 via gen_batch, seed {SEED:#x}",
+            "replica_map": f"{shape_map_name(1)} (reference placement pipeline)",
+            "l2": f"inputs > L2: {wbytes / 1e9:.2f} GB expert weights streamed from HBM every step",
             "parallelism": f"replicas x{args.gpus}"}
+
+
+def shape_map_name(M):
+    return {"c2": "maps/c2.map" if M == 1 else f"maps/c2_m{M}.map", "c3": f"maps/c3_m{M}.map",
+            "c4": "one replica per expert" if M == 1 else f"maps/c4_n{M}.map"}[MAP]
 
 
 def run_ours(args):
@@ -220,8 +263,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     T = args.tokens
 
-    rmap = J.config_map(MAP)
+    rmap, _ = shape_map(J, 1)
     layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=-1, device=local)
+    set_shared_expert(layer, dev)
     w13, w2 = build_weight_store(layer, seed=1)
     layer.set_weights(w13, w2)
     batches = [torch.from_numpy(b).to(dev) for b in gen_batches(T)]
@@ -235,6 +279,8 @@ def run_ours(args):
         a = sched.schedule(J.ActivationBatch(T, K_TOP, b))
         A = int((a.expert_instance >= 0).sum())
         rows = T * K_TOP
+        if SHARED:  # the shared expert: one more weight set, T more rows
+            A, rows = A + 1, rows + T
         alg_bytes.append(A * 3 * D_H * D_E * 2 + rows * (D_H + D_E) * 2 * 2)
         alg_flops.append(6.0 * D_H * D_E * rows)
 
@@ -401,7 +447,7 @@ def run_box(args):
     role = plan.role(rank)
     layer = None
     if role == "moe":
-        rmap = J.config_map(MAP if M == 1 else f"{MAP}_m{M}")
+        rmap, _ = shape_map(J, M)
         layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
     box = JanusBox(plan, rank, T, D_H, K_TOP, layer=layer, device=local,
@@ -575,15 +621,14 @@ def run_box(args):
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (gen_batch Zipf routing, random-init bf16 weights)",
-            "config": {"workload": f"c2 expert shape (Qwen3-30B-A3B: 128 experts, top-8, "
-                                   f"d_h 2048, d_e 768) on one NVLink box split {A} attention + "
+            "config": {"workload": f"{SHAPE_NAME} on one NVLink box split {A} attention + "
                                    f"{M} MoE GPUs; attention->MoE dispatch and MoE->attention "
                                    f"combine by " + ("NVSwitch multicast (NVLS) kernels"
                                                      if box.transport == "nvls"
                                                      else "peer-memory (P2P) kernels"),
                        "transport": box.transport,
                        "tokens_per_step": T, "tokens_per_moe_gpu": args.tokens,
-                       "replica_map": f"maps/{MAP if M == 1 else f'{MAP}_m{M}'}.map",
+                       "replica_map": shape_map_name(M),
                        "parallelism": f"{A}A+{M}E", "l2": "inputs > L2 (weights streamed)"},
             "tokens_per_s_per_gpu": value / ws, "tokens_per_s_per_moe_gpu": value / M,
             "roofline": {"bound": "hbm", "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
@@ -626,10 +671,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shape", default="c2", choices=sorted(SHAPES),
+                    help="expert shape (BASELINE configs); c2 is the headline")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls"],
                     help="box exchange for --gpus > 1 (auto: NVLS multicast when supported)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    apply_shape(args.shape)
     if args.impl == "reference":
         run_reference(args)
     elif dist_env()[0] > 1:
