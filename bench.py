@@ -362,10 +362,19 @@ def run_ours(args):
     gbs = bytes_avg / ffn_s / 1e9
     tfs = flops_avg / ffn_s / 1e12
     hbm_bound = gbs / hbm >= tfs / (tf_sus or tf_burst)
+    # DRAM bytes of the two grouped GEMMs from the committed ncu --set full
+    # capture of this workload (profiles/r1/ncu_traffic.json), per step like
+    # `achieved`'s bytes; null for shapes / sizes not captured
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")
+    if MAP == "c2" and os.path.exists(tpath):
+        tr = json.load(open(tpath)).get(str(T))
+        traffic = tr["grouped_gemm_dram_bytes_per_step"] if tr else None
     roofline = ({"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                 "traffic": None} if hbm_bound else
+                 "traffic": traffic} if hbm_bound else
                 {"bound": "tensor", "achieved": tfs, "peak": tf_sus or tf_burst,
-                 "unit": "TFLOP/s", "frac": tfs / (tf_sus or tf_burst), "traffic": None})
+                 "unit": "TFLOP/s", "frac": tfs / (tf_sus or tf_burst), "traffic": traffic})
+    roofline["traffic_unit"] = "DRAM bytes per step (ncu), vs alg_bytes_per_step"
     roofline.update({"kernel": "grouped_gemm_kernel (gate-up SwiGLU + down), per layer call",
                      "peak_source": f"{src} (MEASURED_PEAKS.json)",
                      "ffn_us_per_step": ffn_s * 1e6,
