@@ -73,7 +73,6 @@ struct GemmParams {
   const int32_t *group_off;
   const int32_t *tile_off;  // n-tiles of tile_n rows per group (prefix)
   unsigned *ctr;            // [2] next-tile counter, finished CTAs (reset by the last CTA)
-  int dbg;
   int tile_n;     // token rows per tile (= 2*BH)
   int q_begin, q_end;
   int K;          // reduction length
@@ -327,7 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int t_next = 0;  // drawn one tile ahead; consumed after this tile
       if (leader && lane == 0) t_next = (int)atomicAdd(p.ctr, 1u);
       const TileCoord c = tile_coord(p, t);
-      const uint32_t bbytes = (p.dbg & 2) ? 0u : 2u * kBK * 2;  // per token row of the pair
+      const uint32_t bbytes = 2u * kBK * 2;  // per token row of the pair
       const uint32_t bytes_pair = 2u * kATileBytes + bbytes * c.half;
       const int rowq = (c.q - p.q_begin) * p.m_per_q;
       for (int kb = 0; kb < kblocks; ++kb) {
@@ -474,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             unsigned char *sb = stage_base + stage * kStageBytes + kATileBytes;
             const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
-            if (!(p.dbg & 2) && elect_one()) {
+            if (elect_one()) {
               // half = 8*m rows: one TMA box per set bit of m, largest first (boxes
               // of 128/64/32/16/8 rows land on 8-row = 1024-B swizzle atoms)
               int off = 0;
@@ -529,7 +528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // CTA 1 rows [half, 2*half) of the sub-tile)
       const int sr0 = c.r0 + sub * p.tile_n;
       const int srows = sub ? c.rows - p.tile_n : min(c.rows, p.tile_n);
-      for (int c0 = grp * kEpiCols; c0 < ((p.dbg & 1) ? 0 : srows); c0 += kEpiGroups * kEpiCols) {
+      for (int c0 = grp * kEpiCols; c0 < srows; c0 += kEpiGroups * kEpiCols) {
         const int rows = min(kEpiCols, srows - c0);
         // Output block of this warp: 32 token rows x kF features (SWIGLU: 16
         // features of h, PLAIN: 32 of y).  The 16x256b TMEM shape hands each
@@ -710,11 +709,6 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   g.group_off = group_off;
   g.tile_off = tile_off;
   g.tile_n = p.tile_n;
-  static const int dbg = [] {
-    const char *e = getenv("JANUS_GEMM_DBG");
-    return e ? atoi(e) : 0;
-  }();
-  g.dbg = dbg;
   g.ctr = p.tile_ctr;
   g.q_begin = p.q_begin;
   g.q_end = p.q_end;
