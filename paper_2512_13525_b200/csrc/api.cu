@@ -449,8 +449,11 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   CK(cudaMemset(ctx->ffn.h, 0, (size_t)S_alloc * d_e * 2));
   CK(dalloc(&ctx->ffn.tile_ctr, 4));
   CK(cudaMemset(ctx->ffn.tile_ctr, 0, 4 * sizeof(unsigned)));
-  CK(alloc_assign(ctx->ws, S, m.E, m.N, m.R));
-  CK(dalloc(&ctx->ws_tile_off, m.R + 1));
+  // per-map arrays at the build's limits: a later janus_set_replica_map
+  // (reconfiguration) may grow E / N / R without a reconfigure
+  (void)m;
+  CK(alloc_assign(ctx->ws, S, JANUS_MAX_EXPERTS, JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
+  CK(dalloc(&ctx->ws_tile_off, JANUS_MAX_REPLICAS + 1));
   CK(cudaMalloc(&ctx->d_x, (size_t)max_tokens * d_h * 2));
   CK(cudaMalloc(&ctx->d_outbuf, (size_t)max_tokens * d_h * 2));
   CK(dalloc(&ctx->d_experts, S));

@@ -34,13 +34,24 @@ class MoELayer:
         st = lib.janus_moe_configure(self.ctx, d_hidden, d_expert, max_tokens, top_k)
         if st != OK:
             raise JanusError(st, self.sched.last_error())
+        self._derive_order()
+        self.w13 = self.w2 = None
+
+    def _derive_order(self):
         self.qidx, self.qbase = self.sched.replica_order()
         off, _, _ = self.sched._csr
         # expert held at each replica-order index q
         self.q_expert = np.zeros(int(off[-1]), np.int32)
-        for e in range(rmap.num_experts):
+        for e in range(self.map.num_experts):
             for p in range(off[e], off[e + 1]):
                 self.q_expert[self.qidx[p]] = e
+
+    def set_map(self, rmap: ReplicaMap) -> None:
+        """Replica-map reconfiguration: re-upload the CSR; the
+        weight store must be set again (replica order changes)."""
+        self.sched.set_map(rmap)
+        self.map = rmap
+        self._derive_order()
         self.w13 = self.w2 = None
 
     @property

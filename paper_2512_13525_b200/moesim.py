@@ -188,6 +188,18 @@ class Scheduler:
         if st != OK:
             raise JanusError(st, self.last_error())
 
+    def set_map(self, rmap: ReplicaMap) -> None:
+        """Reconfiguration: upload a new replica map (janus_set_replica_map)."""
+        off, hosts, rid = rmap.csr()
+        st = lib.janus_set_replica_map(self.ctx, rmap.num_experts, rmap.num_instances,
+                                       rmap.slots_per_instance, _ptr(off), _ptr(hosts), _ptr(rid))
+        if st == EINVAL:
+            raise ValidationError(self.last_error())
+        if st != OK:
+            raise JanusError(st, self.last_error())
+        self.map = rmap
+        self._csr = (off, hosts, rid)
+
     def last_error(self) -> str:
         return lib.janus_last_error(self.ctx).decode()
 

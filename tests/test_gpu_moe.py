@@ -279,3 +279,22 @@ def test_deepseek_v3_shape_with_shared_expert_sampled_tokens(J, oracle):
     xs = u16(x)[tokens]
     ref += oracle.expert_swiglu(xs, u16(wg), u16(wu), u16(wd), round_h=True, nthreads=8)
     check_close(bf16_to_f32(u16(out))[tokens], ref, "DS-V3 shape + shared")
+
+
+def test_replica_map_reconfiguration(J, oracle):
+    """Replica-map lifecycle (§8(f) 3): a configured layer takes a new map with
+    more experts, instances and replicas (janus_set_replica_map re-uploads the
+    CSR; the weight store is set again) and stays exact."""
+    from paper_2512_13525_b200.moe import build_weight_store
+    small = J.ReplicaMap.from_hosts(1, 8, [[0]] * 8)
+    layer = make_layer(J, small, 256, 128, 200, 4)
+    b = J.gen_batch(J.RoutingPattern.uniform(8), 150, 4, 1, 0)
+    x, ex, gw, out = run(J, layer, b.experts, 150)
+    check_close(bf16_to_f32(u16(out)), oracle_layer_out(oracle, layer, x, ex, gw), "before")
+    hosts = [sorted({e % 3, (e * 7) % 3}) for e in range(48)]
+    big = J.ReplicaMap.from_hosts(3, 48, hosts)
+    layer.set_map(big)
+    layer.set_weights(*build_weight_store(layer, seed=2))
+    b = J.gen_batch(J.RoutingPattern.zipf(48, 1.0), 200, 4, 2, 0)
+    x, ex, gw, out = run(J, layer, b.experts, 200)
+    check_close(bf16_to_f32(u16(out)), oracle_layer_out(oracle, layer, x, ex, gw), "after")
