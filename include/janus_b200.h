@@ -215,7 +215,10 @@ janus_status janus_xfer_handle(const janus_ctx *ctx, uint8_t *handle /* 64 bytes
 janus_status janus_xfer_connect(janus_ctx *ctx, const uint8_t *handles /* world x 64, by rank */);
 /* device, attention rank a: push this rank's shard (janus_shard_tokens of the
  * step's num_tokens) — rows x [T_a][d_h] bf16, experts / gate_w [T_a*k] — into
- * every MoE rank, then publish `epoch` (> 0, increasing per step). */
+ * every MoE rank, then publish `epoch` (> 0, increasing per step).  With both
+ * routing pointers NULL only the rows move: the MoE ranks gate themselves
+ * (janus_moe_set_router on their contexts; Janus gates on the MoE side,
+ * PAPER.md:671-678). */
 janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                                        const float *d_gate_w, int64_t num_tokens, uint64_t epoch,
                                        void *stream);

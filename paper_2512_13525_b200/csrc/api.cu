@@ -746,6 +746,8 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
   if (x.rank >= x.A) return fail(ctx, JANUS_EINVAL, "xfer: dispatch from a non-attention rank");
   if (T < 0 || T > x.T_max || epoch == 0)
     return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens] or epoch 0");
+  if (!d_experts != !d_gate_w)
+    return fail(ctx, JANUS_EINVAL, "xfer: pass both routing arrays, or neither (MoE-side gating)");
   cudaError_t e = janus::launch_dispatch(x, d_x, d_experts, d_gate_w, T, epoch,
                                          static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(ctx, e, "dispatch_kernel");
@@ -764,6 +766,16 @@ janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoc
   cudaError_t e = janus::launch_wait(x, true, epoch, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
   ctx->launches += 1;
+  if (ctx->router) {  // MoE-side gating: routing from the received rows
+    unsigned char *base =
+        x.mc ? reinterpret_cast<unsigned char *>(x.uc_va) + janus::xfer_slot(epoch) * x.mslot
+             : static_cast<unsigned char *>(x.local) + janus::xfer_slot(epoch) * x.L.slot_stride;
+    const void *xr = base + (x.mc ? x.mx_off : x.L.x_off);
+    janus_status gs = janus_gate_async(ctx, xr, ctx->router, T, ctx->d_h, ctx->dmap.E,
+                                       ctx->top_k, ctx->d_experts, ctx->d_gw, stream);
+    if (gs != JANUS_OK) return gs;
+    return layer_run(ctx, xr, ctx->d_experts, ctx->d_gw, (int)T, nullptr, nullptr, s, epoch);
+  }
   if (x.mc) {  // rows / routing landed in this rank's multicast backing
     unsigned char *base = reinterpret_cast<unsigned char *>(x.uc_va) + janus::xfer_slot(epoch) * x.mslot;
     return layer_run(ctx, base + x.mx_off, reinterpret_cast<const int32_t *>(base + x.mex_off),

@@ -122,7 +122,9 @@ __global__ void dispatch_kernel(DispatchDst dst, PeerPtrs peers, int M, int A, i
       }
     }
   }
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ns; i += stride) {
+  // routing rows (absent when the MoE side gates: it computes them from x)
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; ex && i < ns;
+       i += stride) {
     const int32_t e = __ldg(ex + i);
     const float w = __ldg(gw + i);
     for (int g = 0; g < dst.n; ++g) {

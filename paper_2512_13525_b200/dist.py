@@ -173,10 +173,12 @@ class JanusBox:
     # --- attention rank ------------------------------------------------------
     def dispatch(self, x_shard, experts_shard, gate_w_shard, num_tokens: int, epoch: int,
                  stream: int) -> None:
-        self._check(lib.janus_attn_dispatch_async(self._ctx, x_shard.data_ptr(),
-                                                  experts_shard.data_ptr(),
-                                                  gate_w_shard.data_ptr(), num_tokens, epoch,
-                                                  stream))
+        """experts / gate_w None: rows only, the MoE ranks gate (set_router)."""
+        self._check(lib.janus_attn_dispatch_async(
+            self._ctx, x_shard.data_ptr(),
+            experts_shard.data_ptr() if experts_shard is not None else None,
+            gate_w_shard.data_ptr() if gate_w_shard is not None else None, num_tokens, epoch,
+            stream))
 
     def combine(self, out_shard, num_tokens: int, epoch: int, stream: int) -> None:
         self._check(lib.janus_attn_combine_async(self._ctx, out_shard.data_ptr(), num_tokens,

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--out", default="gpurun_out")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls"])
     ap.add_argument("--shared", action="store_true", help="add a shared expert (NVLS only)")
+    ap.add_argument("--gate", action="store_true",
+                    help="MoE-side gating: dispatch rows only, MoE ranks run the router")
     ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
                     help="2: dispatch step s+1 before combining step s (double-buffered slots)")
     args = ap.parse_args()
@@ -57,6 +59,11 @@ def main():
         shared_w = (torch.cat([wg, wu]).contiguous(), wd.contiguous())
         if layer is not None:
             layer.set_shared(*shared_w)
+    if args.gate:
+        from paper_2512_13525_b200.moe import router_weights
+        wr = router_weights(E, d_h, 13, dev)
+        if layer is not None:
+            layer.set_router(wr)
     box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local, transport=args.transport)
     full = None
     if plan.role(rank) == "attention":
@@ -64,6 +71,8 @@ def main():
         full.set_weights(*build_weight_store(full, seed=1))
         if args.shared:
             full.set_shared(*shared_w)
+        if args.gate:
+            full.set_router(wr)
 
     stream = torch.cuda.current_stream(dev).cuda_stream
     result = {"rank": rank, "role": plan.role(rank), "steps": [], "transport": box.transport}
@@ -81,8 +90,12 @@ def main():
         def dispatch(step):
             Ts, x, gw, ex = steps[step - 1]
             first, cnt = plan.shard(Ts, rank)
-            box.dispatch(x[first:first + cnt].contiguous(), ex[first * k:(first + cnt) * k].contiguous(),
-                         gw[first * k:(first + cnt) * k].contiguous(), Ts, step, stream)
+            if args.gate:
+                box.dispatch(x[first:first + cnt].contiguous(), None, None, Ts, step, stream)
+            else:
+                box.dispatch(x[first:first + cnt].contiguous(),
+                             ex[first * k:(first + cnt) * k].contiguous(),
+                             gw[first * k:(first + cnt) * k].contiguous(), Ts, step, stream)
 
         def combine(step):
             Ts = steps[step - 1][0]
@@ -105,7 +118,7 @@ def main():
         for step in range(1, args.steps + 1):
             Ts, x, gw, ex = steps[step - 1]
             first, cnt = plan.shard(Ts, rank)
-            ref = full.forward(x, ex, gw)[first:first + cnt]
+            ref = (full.forward_gated(x) if args.gate else full.forward(x, ex, gw))[first:first + cnt]
             torch.cuda.synchronize()
             o, r = outs[step].float().cpu().numpy(), ref.float().cpu().numpy()
             rms = float(np.sqrt(np.mean(r.astype(np.float64) ** 2))) or 1.0
@@ -119,7 +132,7 @@ def main():
         torch.cuda.synchronize()
     result["timed_out"] = box.timed_out()
     os.makedirs(args.out, exist_ok=True)
-    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}_rank{rank}.json"), "w") as f:
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}{'g' if args.gate else ''}_rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
     dist.destroy_process_group()

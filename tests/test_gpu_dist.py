@@ -42,17 +42,21 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
                 assert s["bad"] == 0, s
 
 
-def test_box_exchange_with_shared_expert():
-    """The shared expert in a box: MoE instance 0 adds it to its partials
-    (NVLS transport, two steps in flight)."""
+@pytest.mark.parametrize("flag", ["--shared", "--gate"])
+def test_box_exchange_shared_expert_and_moe_side_gating(flag):
+    """--shared: the shared expert in a box (MoE instance 0 adds it to its
+    partials).  --gate: rows only are dispatched and every MoE rank computes
+    the routing with the gating kernel (Janus gates on the MoE side).  NVLS
+    transport, two steps in flight."""
     attn, moe = 1, 3
     if gpus() < attn + moe:
         pytest.skip(f"needs {attn + moe} GPUs (one rank per GPU)")
     out = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={attn + moe}", "--master-addr", "127.0.0.1", "--master-port",
-           "29777", os.path.join(ROOT, "tests", "dist_worker.py"), "--attn", str(attn), "--moe",
-           str(moe), "--out", out, "--transport", "nvls", "--inflight", "2", "--shared"]
+           str(29777 + (flag == "--gate")), os.path.join(ROOT, "tests", "dist_worker.py"),
+           "--attn", str(attn), "--moe",
+           str(moe), "--out", out, "--transport", "nvls", "--inflight", "2", flag]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
