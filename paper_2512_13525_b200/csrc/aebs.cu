@@ -285,18 +285,27 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   if (trace && tid == 0) trace[2] = globaltimer();
 
   // ---- the one cluster exchange: totals and bad ids via DSMEM ---------------
-  cluster.sync();
   int bad = INT_MAX;
-  for (int c = 0; c < csize; ++c) bad = min(bad, *cluster.map_shared_rank(&s_bad, c));
-  for (int e = tid; e < E; e += kSchedThreads) {
-    int before = 0, all = 0;
-    for (int c = 0; c < csize; ++c) {
-      const int v = *cluster.map_shared_rank(ltot + e, c);
-      before += c < crank ? v : 0;
-      all += v;
+  if (csize == 1) {  // no peers: local smem only
+    __syncthreads();
+    bad = s_bad;
+    for (int e = tid; e < E; e += kSchedThreads) {
+      xbase[e] = 0;
+      tot[e] = ltot[e];
     }
-    xbase[e] = before;
-    tot[e] = all;
+  } else {
+    cluster.sync();
+    for (int c = 0; c < csize; ++c) bad = min(bad, *cluster.map_shared_rank(&s_bad, c));
+    for (int e = tid; e < E; e += kSchedThreads) {
+      int before = 0, all = 0;
+      for (int c = 0; c < csize; ++c) {
+        const int v = *cluster.map_shared_rank(ltot + e, c);
+        before += c < crank ? v : 0;
+        all += v;
+      }
+      xbase[e] = before;
+      tot[e] = all;
+    }
   }
   cluster_arrive();  // our reads of remote smem are done (wait before exit)
   if (bad != INT_MAX) {
