@@ -450,12 +450,12 @@ def run_box(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    plan = BoxPlan.for_gpus(ws)
+    plan = BoxPlan.moe_only(ws) if args.box == "moe-only" else BoxPlan.for_gpus(ws)
     A, M = plan.n_attn, plan.n_moe
     T = args.tokens * M
-    role = plan.role(rank)
+    att, moe = plan.is_attention(rank), plan.is_moe(rank)
     layer = None
-    if role == "moe":
+    if moe:
         rmap, _ = shape_map(J, M)
         layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
@@ -465,30 +465,35 @@ def run_box(args):
     batches = [torch.from_numpy(J.gen_batch(pat, T, K_TOP, SEED, T * 1000 + i).experts).to(dev)
                for i in range(N_BATCHES)]
     x, gw = make_inputs(T, K_TOP, D_H, 3, dev)
-    first, cnt = plan.shard(T, rank) if role == "attention" else (0, 0)
+    first, cnt = plan.shard(T, rank) if att else (0, 0)
     xs = x[first:first + cnt].contiguous()
-    gws = [gw[first * K_TOP:(first + cnt) * K_TOP].contiguous()] if role == "attention" else []
+    gws = [gw[first * K_TOP:(first + cnt) * K_TOP].contiguous()] if att else []
     exs = [b[first * K_TOP:(first + cnt) * K_TOP].contiguous() for b in batches]
     out = torch.empty(max(cnt, 1), D_H, dtype=torch.bfloat16, device=dev)
     s = torch.cuda.current_stream(dev)
     stream = s.cuda_stream
+    # a colocated rank runs its MoE role on a second stream (NVLS transport:
+    # the two roles share no device state), so its combine of step i — which
+    # waits for every rank's MoE step i — does not hold back its MoE step i+1
+    s_moe = torch.cuda.Stream(dev) if (plan.colocated and box.transport == "nvls") else s
+    stream_moe = s_moe.cuda_stream
     epoch = [0]
 
     # Two steps in flight (the exchange double-buffers by epoch parity): an
     # attention rank dispatches step i+1 before it combines step i, so the MoE
     # GPUs find step i+1's rows already delivered when they finish step i.
+    # (a colocated rank interleaves its two roles in that order on one stream)
     def run_steps(n, i0=0):
         e0_ = epoch[0]
-        if role == "attention":
+        if att:
             box.dispatch(xs, exs[i0 % N_BATCHES], gws[0], T, e0_ + 1, stream)
-            for j in range(n):
-                if j + 1 < n:
-                    box.dispatch(xs, exs[(i0 + j + 1) % N_BATCHES], gws[0], T, e0_ + j + 2,
-                                 stream)
+        for j in range(n):
+            if att and j + 1 < n:
+                box.dispatch(xs, exs[(i0 + j + 1) % N_BATCHES], gws[0], T, e0_ + j + 2, stream)
+            if moe:
+                box.moe_step(T, e0_ + j + 1, stream_moe)
+            if att:
                 box.combine(out, T, e0_ + j + 1, stream)
-        else:
-            for j in range(n):
-                box.moe_step(T, e0_ + j + 1, stream)
         epoch[0] += n
 
     run_steps(args.warmup)
@@ -521,7 +526,7 @@ def run_box(args):
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     for i in range(nd):
         epoch[0] += 1
-        if role == "attention":
+        if att:
             d0, d1 = ev(), ev()
             d0.record(s)
             box.dispatch(xs, exs[i % N_BATCHES], gws[0], T, epoch[0], stream)
@@ -529,15 +534,15 @@ def run_box(args):
             torch.cuda.synchronize()
             disp_ms += d0.elapsed_time(d1) / nd
         dist.barrier()
-        if role == "moe":
+        if moe:
             m0, m1 = ev(), ev()
-            m0.record(s)
-            box.moe_step(T, epoch[0], stream)
-            m1.record(s)
+            m0.record(s_moe)
+            box.moe_step(T, epoch[0], stream_moe)
+            m1.record(s_moe)
             torch.cuda.synchronize()
             moe_ms += m0.elapsed_time(m1) / nd
         dist.barrier()
-        if role == "attention":
+        if att:
             c0, c1 = ev(), ev()
             c0.record(s)
             box.combine(out, T, epoch[0], stream)
@@ -558,7 +563,7 @@ def run_box(args):
 
     # e2e through the host API: attention ranks copy their shard in from pinned
     # host memory and their outputs back each step
-    if role == "attention":
+    if att:
         xh = xs.cpu().pin_memory()
         exh = [e.cpu().pin_memory() for e in exs]
         gwh = gws[0].cpu().pin_memory()
@@ -567,7 +572,7 @@ def run_box(args):
     dist.barrier()
     t0 = time.perf_counter()
     e0_ = epoch[0]
-    if role == "attention":
+    if att:
         # per step: H2D of step i+1's shard (copy stream), dispatch i+1,
         # combine i (compute stream), D2H of step i's output (second copy
         # stream) — every step's bytes cross PCIe, overlapped with the layer
@@ -598,6 +603,8 @@ def run_box(args):
         for i in range(args.steps):
             if i + 1 < args.steps:
                 h2d_dispatch(i + 1)
+            if moe:  # colocated rank: its MoE role for step i
+                box.moe_step(T, e0_ + i + 1, stream_moe)
             b = i & 1
             if i >= 2:
                 s.wait_event(ev_read[b])
@@ -630,15 +637,20 @@ def run_box(args):
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (gen_batch Zipf routing, random-init bf16 weights)",
-            "config": {"workload": f"{SHAPE_NAME} on one NVLink box split {A} attention + "
-                                   f"{M} MoE GPUs; attention->MoE dispatch and MoE->attention "
-                                   f"combine by " + ("NVSwitch multicast (NVLS) kernels"
+            "config": {"workload": f"{SHAPE_NAME} on one NVLink box " +
+                                   (f"of {M} GPUs each owning a token shard and an MoE instance "
+                                    f"(MoE-only box); token dispatch and combine "
+                                    if plan.colocated else
+                                    f"split {A} attention + {M} MoE GPUs; attention->MoE "
+                                    f"dispatch and MoE->attention ") +
+                                   "combine by " + ("NVSwitch multicast (NVLS) kernels"
                                                      if box.transport == "nvls"
                                                      else "peer-memory (P2P) kernels"),
                        "transport": box.transport,
                        "tokens_per_step": T, "tokens_per_moe_gpu": args.tokens,
                        "replica_map": shape_map_name(M),
-                       "parallelism": f"{A}A+{M}E", "l2": "inputs > L2 (weights streamed)"},
+                       "parallelism": f"{M} x (A+E)" if plan.colocated else f"{A}A+{M}E",
+                       "l2": "inputs > L2 (weights streamed)"},
             "tokens_per_s_per_gpu": value / ws, "tokens_per_s_per_moe_gpu": value / M,
             "roofline": {"bound": "hbm", "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
                          "ffn_us_per_step": ffn_ms * 1e3, "achieved": None, "peak": hbm,
@@ -680,6 +692,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--box", default="split", choices=["split", "moe-only"],
+                    help="--gpus > 1: the paper's attention/MoE split (1 attention GPU per "
+                         "4), or the MoE-only box (every GPU owns tokens and experts)")
     ap.add_argument("--shape", default="c2", choices=sorted(SHAPES),
                     help="expert shape (BASELINE configs); c2 is the headline")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls"],

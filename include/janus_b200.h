@@ -211,6 +211,11 @@ void janus_shard_tokens(int64_t num_tokens, int attn_instances, int a, int64_t *
  * then maps all peers' regions (CUDA IPC over NVLink P2P). */
 janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int rank,
                                   int max_tokens, int d_hidden, int top_k);
+/* The MoE-only box (SURVEY §8(e) "c4 N=4 MoE-only"): all n ranks own a token
+ * shard AND are MoE instances g = rank; every dispatch / MoE / combine call
+ * below is then legal on every rank. */
+janus_status janus_xfer_configure_colocated(janus_ctx *ctx, int n, int rank, int max_tokens,
+                                            int d_hidden, int top_k);
 janus_status janus_xfer_handle(const janus_ctx *ctx, uint8_t *handle /* 64 bytes */);
 janus_status janus_xfer_connect(janus_ctx *ctx, const uint8_t *handles /* world x 64, by rank */);
 /* device, attention rank a: push this rank's shard (janus_shard_tokens of the

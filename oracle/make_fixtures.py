@@ -46,7 +46,9 @@ CONFIGS = {
     # C = ceil(1.25 * E / M) as in c3's 6 x 27)
     "c2_m2": dict(kind="zipf", E=128, k=8, N=2, C=80, seed=0x30, s=1.0),
     "c2_m3": dict(kind="zipf", E=128, k=8, N=3, C=54, seed=0x30, s=1.0),
+    "c2_m4": dict(kind="zipf", E=128, k=8, N=4, C=40, seed=0x30, s=1.0),
     "c2_m6": dict(kind="zipf", E=128, k=8, N=6, C=27, seed=0x30, s=1.0),
+    "c2_m8": dict(kind="zipf", E=128, k=8, N=8, C=20, seed=0x30, s=1.0),
     "c3_m1": dict(kind="zipf", E=128, k=8, N=1, C=128, seed=0x235, s=1.0),
     "c3_m2": dict(kind="zipf", E=128, k=8, N=2, C=80, seed=0x235, s=1.0),
     "c3_m3": dict(kind="zipf", E=128, k=8, N=3, C=54, seed=0x235, s=1.0),

@@ -676,13 +676,14 @@ janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_
 
 // ------------------------------------------------ box exchange (K6) -----
 
-janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int rank, int max_tokens,
-                                  int d_h, int k) {
+static janus_status xfer_setup(janus_ctx *ctx, int n_attn, int n_moe, int rank, int max_tokens,
+                               int d_h, int k, bool colocated) {
   if (!ctx) return JANUS_EINVAL;
-  if (n_attn < 1 || n_moe < 1 || rank < 0 || rank >= n_attn + n_moe || max_tokens < 1 ||
-      d_h <= 0 || d_h % 8 || k < 1)
+  const int world = colocated ? n_attn : n_attn + n_moe;
+  if (n_attn < 1 || n_moe < 1 || rank < 0 || rank >= world || max_tokens < 1 || d_h <= 0 ||
+      d_h % 8 || k < 1)
     return fail(ctx, JANUS_EINVAL, "xfer: bad configuration");
-  if (n_attn + n_moe > 16 || n_moe > 32)
+  if (world > 16 || n_moe > 32)
     return fail(ctx, JANUS_EUNSUPPORTED, "xfer: at most 16 ranks in one box");
   CK(cudaSetDevice(ctx->device));
   janus::XferState &x = ctx->xfer;
@@ -693,7 +694,8 @@ janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int ran
   dfree(x.err);
   x = janus::XferState{};
   x.rank = rank;
-  x.world = n_attn + n_moe;
+  x.world = world;
+  x.moe0 = colocated ? 0 : n_attn;
   x.A = n_attn;
   x.M = n_moe;
   x.d_h = d_h;
@@ -710,6 +712,16 @@ janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int ran
   x.peer_base[rank] = x.local;
   ctx->xfer_ready = false;
   return JANUS_OK;
+}
+
+janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int rank, int max_tokens,
+                                  int d_h, int k) {
+  return xfer_setup(ctx, n_attn, n_moe, rank, max_tokens, d_h, k, false);
+}
+
+janus_status janus_xfer_configure_colocated(janus_ctx *ctx, int n, int rank, int max_tokens,
+                                            int d_h, int k) {
+  return xfer_setup(ctx, n, n, rank, max_tokens, d_h, k, true);
 }
 
 janus_status janus_xfer_handle(const janus_ctx *ctx, uint8_t *handle) {
@@ -758,7 +770,7 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
 janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoch, void *stream) {
   if (!ctx || !ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: not connected");
   const janus::XferState &x = ctx->xfer;
-  if (x.rank < x.A || ctx->instance != x.rank - x.A)
+  if (x.rank < x.moe0 || ctx->instance != x.rank - x.moe0)
     return fail(ctx, JANUS_EINVAL, "xfer: MoE rank must hold instance rank - n_attn");
   if (T < 0 || T > x.T_max || epoch == 0)
     return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens] or epoch 0");

@@ -108,6 +108,9 @@ XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k);
 
 struct XferState {
   int rank = -1, world = 0, A = 0, M = 0, d_h = 0, k = 0;
+  // first MoE rank: A for a split box; 0 when every rank is both an attention
+  // shard owner and an MoE instance (janus_xfer_configure_colocated)
+  int moe0 = 0;
   long long T_max = 0;
   XferLayout L{};
   void *local = nullptr;              // this rank's exchange region

@@ -95,7 +95,7 @@ struct DispatchDst {
   size_t x_off, ex_off, gw_off;
 };
 
-__global__ void dispatch_kernel(DispatchDst dst, PeerPtrs peers, int M, int A, int a,
+__global__ void dispatch_kernel(DispatchDst dst, PeerPtrs peers, int M, int moe0, int a,
                                 const uint4 *__restrict__ x, const int32_t *__restrict__ ex,
                                 const float *__restrict__ gw, long long first, long long Ta,
                                 int vec, int k, XferLayout L, unsigned long long epoch,
@@ -134,7 +134,8 @@ __global__ void dispatch_kernel(DispatchDst dst, PeerPtrs peers, int M, int A, i
   }
   if (last_block(counter) && threadIdx.x < M) {
     unsigned long long *flag =
-        reinterpret_cast<unsigned long long *>(peers.base[A + threadIdx.x] + L.flag_dispatch_off) + a;
+        reinterpret_cast<unsigned long long *>(peers.base[moe0 + threadIdx.x] + L.flag_dispatch_off) +
+        a;
     st_release_sys(flag, epoch);
   }
 }
@@ -343,14 +344,15 @@ cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *
     dst.gw_off = x.mgw_off + so;
   } else {
     const size_t so = xfer_slot(epoch) * x.L.slot_stride;
-    for (int g = 0; g < x.M; ++g) dst.base[g] = static_cast<unsigned char *>(x.peer_base[x.A + g]);
+    for (int g = 0; g < x.M; ++g)
+      dst.base[g] = static_cast<unsigned char *>(x.peer_base[x.moe0 + g]);
     dst.n = x.M;
     dst.x_off = x.L.x_off + so;
     dst.ex_off = x.L.ex_off + so;
     dst.gw_off = x.L.gw_off + so;
   }
   dispatch_kernel<<<grid_for(std::max<long long>(Ta * vec, 1)), 256, 0, s>>>(
-      dst, peer_ptrs(x), x.M, x.A, a, reinterpret_cast<const uint4 *>(d_x), d_ex, d_gw, first, Ta,
+      dst, peer_ptrs(x), x.M, x.moe0, a, reinterpret_cast<const uint4 *>(d_x), d_ex, d_gw, first, Ta,
       vec, x.k, x.L, epoch, x.counter);
   return cudaGetLastError();
 }
@@ -367,7 +369,7 @@ cudaError_t launch_wait(const XferState &x, bool dispatch_flags, unsigned long l
 cudaError_t launch_combine_push(const XferState &x, const void *y, const int32_t *slot_row,
                                 const int32_t *slot_inst, const float *gw, long long T,
                                 unsigned long long epoch, cudaStream_t s) {
-  const int g = x.rank - x.A;
+  const int g = x.rank - x.moe0;
   combine_push_kernel<<<grid_for(std::max<long long>(T * (x.d_h / 8), 1)), 256, 0, s>>>(
       peer_ptrs(x), x.A, g, reinterpret_cast<const __nv_bfloat16 *>(y), slot_row, slot_inst, gw,
       T, x.k, x.d_h, x.L.ta_max, x.L, x.L.part_off + xfer_slot(epoch) * x.L.slot_stride, epoch,
@@ -388,7 +390,7 @@ cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta
 }
 
 cudaError_t launch_signal_combine(const XferState &x, unsigned long long epoch, cudaStream_t s) {
-  signal_combine_kernel<<<1, 32, 0, s>>>(peer_ptrs(x), x.A, x.rank - x.A, x.L, epoch);
+  signal_combine_kernel<<<1, 32, 0, s>>>(peer_ptrs(x), x.A, x.rank - x.moe0, x.L, epoch);
   return cudaGetLastError();
 }
 

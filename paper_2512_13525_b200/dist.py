@@ -28,24 +28,37 @@ from .moesim import JanusError, shard_tokens
 
 @dataclass(frozen=True)
 class BoxPlan:
-    """Roles and token ownership of an A-attention + M-MoE box (pure host logic)."""
+    """Roles and token ownership of an A-attention + M-MoE box (pure host logic).
+    ``colocated``: the MoE-only box — every rank owns a token shard and is MoE
+    instance ``rank`` (n_attn == n_moe == world)."""
 
     n_attn: int
     n_moe: int
+    colocated: bool = False
 
     @property
     def world(self) -> int:
-        return self.n_attn + self.n_moe
+        return self.n_attn if self.colocated else self.n_attn + self.n_moe
 
     def role(self, rank: int) -> str:
+        if self.colocated:
+            return "both"
         return "attention" if rank < self.n_attn else "moe"
 
+    def is_attention(self, rank: int) -> bool:
+        return self.colocated or rank < self.n_attn
+
+    def is_moe(self, rank: int) -> bool:
+        return self.colocated or rank >= self.n_attn
+
     def instance(self, rank: int) -> int:
+        if self.colocated:
+            return rank
         return rank - self.n_attn if rank >= self.n_attn else -1
 
     def shard(self, num_tokens: int, rank: int):
         """(first, count) of attention rank's token shard (comm.cpp:76-81)."""
-        assert rank < self.n_attn
+        assert self.is_attention(rank)
         return shard_tokens(num_tokens, self.n_attn, rank)
 
     def owner(self, num_tokens: int, t: int) -> int:
@@ -72,6 +85,10 @@ class BoxPlan:
         a = max(1, n // 4)
         return BoxPlan(a, n - a)
 
+    @staticmethod
+    def moe_only(n: int) -> "BoxPlan":
+        return BoxPlan(n, n, colocated=True)
+
 
 class _Ctx:
     """A bare device context (attention ranks hold no replica map)."""
@@ -97,7 +114,7 @@ class JanusBox:
         import torch.distributed as dist
         self.plan, self.rank = plan, rank
         self.max_tokens, self.d_h, self.k = max_tokens, d_hidden, top_k
-        if plan.role(rank) == "moe":
+        if plan.is_moe(rank):
             if layer is None or layer.instance != plan.instance(rank):
                 raise ValueError("an MoE rank needs its MoELayer with instance = rank - n_attn")
             self.layer = layer
@@ -108,8 +125,12 @@ class JanusBox:
             self._c = _Ctx(device)
             self._ctx = self._c.ctx
             self._err = self._c.last_error
-        self._check(lib.janus_xfer_configure(self._ctx, plan.n_attn, plan.n_moe, rank, max_tokens,
-                                             d_hidden, top_k))
+        if plan.colocated:
+            self._check(lib.janus_xfer_configure_colocated(self._ctx, plan.world, rank, max_tokens,
+                                                           d_hidden, top_k))
+        else:
+            self._check(lib.janus_xfer_configure(self._ctx, plan.n_attn, plan.n_moe, rank,
+                                                 max_tokens, d_hidden, top_k))
         h = C.create_string_buffer(64)
         self._check(lib.janus_xfer_handle(self._ctx, h))
         handles = [None] * plan.world

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--out", default="gpurun_out")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls"])
     ap.add_argument("--shared", action="store_true", help="add a shared expert (NVLS only)")
+    ap.add_argument("--colocated", action="store_true",
+                    help="MoE-only box: every rank owns a shard and is an MoE instance")
     ap.add_argument("--gate", action="store_true",
                     help="MoE-side gating: dispatch rows only, MoE ranks run the router")
     ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
@@ -41,7 +43,7 @@ def main():
     rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    plan = BoxPlan(args.attn, args.moe)
+    plan = BoxPlan.moe_only(args.moe) if args.colocated else BoxPlan(args.attn, args.moe)
     assert dist.get_world_size() == plan.world
     E, k, d_h, d_e, T = 16, 4, 256, 128, args.tokens
     M = plan.n_moe
@@ -50,7 +52,8 @@ def main():
     dev = torch.device("cuda", local)
 
     layer = None
-    if plan.role(rank) == "moe":
+    att, moe = plan.is_attention(rank), plan.is_moe(rank)
+    if moe:
         layer = MoELayer(rmap, d_h, d_e, T, k, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
     if args.shared:
@@ -66,7 +69,7 @@ def main():
             layer.set_router(wr)
     box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local, transport=args.transport)
     full = None
-    if plan.role(rank) == "attention":
+    if att:
         full = MoELayer(rmap, d_h, d_e, T, k, instance=-1, device=local)
         full.set_weights(*build_weight_store(full, seed=1))
         if args.shared:
@@ -84,55 +87,62 @@ def main():
         ex = torch.from_numpy(b.experts).to(dev)
         steps.append((Ts, x, gw, ex))
 
-    if plan.role(rank) == "attention":
-        outs = {}
+    outs = {}
 
-        def dispatch(step):
-            Ts, x, gw, ex = steps[step - 1]
-            first, cnt = plan.shard(Ts, rank)
-            if args.gate:
-                box.dispatch(x[first:first + cnt].contiguous(), None, None, Ts, step, stream)
-            else:
-                box.dispatch(x[first:first + cnt].contiguous(),
-                             ex[first * k:(first + cnt) * k].contiguous(),
-                             gw[first * k:(first + cnt) * k].contiguous(), Ts, step, stream)
-
-        def combine(step):
-            Ts = steps[step - 1][0]
-            first, cnt = plan.shard(Ts, rank)
-            outs[step] = torch.empty(cnt, d_h, dtype=torch.bfloat16, device=dev)
-            box.combine(outs[step], Ts, step, stream)
-
-        if args.inflight == 1:
-            for step in range(1, args.steps + 1):
-                dispatch(step)
-                combine(step)
-                torch.cuda.synchronize()
+    def dispatch(step):
+        Ts, x, gw, ex = steps[step - 1]
+        first, cnt = plan.shard(Ts, rank)
+        if args.gate:
+            box.dispatch(x[first:first + cnt].contiguous(), None, None, Ts, step, stream)
         else:
-            dispatch(1)
-            for step in range(1, args.steps + 1):
-                if step < args.steps:
-                    dispatch(step + 1)
+            box.dispatch(x[first:first + cnt].contiguous(),
+                         ex[first * k:(first + cnt) * k].contiguous(),
+                         gw[first * k:(first + cnt) * k].contiguous(), Ts, step, stream)
+
+    def combine(step):
+        Ts = steps[step - 1][0]
+        first, cnt = plan.shard(Ts, rank)
+        outs[step] = torch.empty(cnt, d_h, dtype=torch.bfloat16, device=dev)
+        box.combine(outs[step], Ts, step, stream)
+
+    # one stream per rank; a colocated rank interleaves its roles in the same
+    # order as the split box's ranks would (dispatch before MoE before combine)
+    if args.inflight == 1:
+        for step in range(1, args.steps + 1):
+            if att:
+                dispatch(step)
+            if moe:
+                box.moe_step(steps[step - 1][0], step, stream)
+            if att:
                 combine(step)
             torch.cuda.synchronize()
-        for step in range(1, args.steps + 1):
-            Ts, x, gw, ex = steps[step - 1]
-            first, cnt = plan.shard(Ts, rank)
-            ref = (full.forward_gated(x) if args.gate else full.forward(x, ex, gw))[first:first + cnt]
-            torch.cuda.synchronize()
-            o, r = outs[step].float().cpu().numpy(), ref.float().cpu().numpy()
-            rms = float(np.sqrt(np.mean(r.astype(np.float64) ** 2))) or 1.0
-            bad = int((np.abs(o - r) > RTOL * np.abs(r) + ATOL * rms).sum())
-            result["steps"].append({"T": Ts, "shard": [first, cnt], "bad": bad,
-                                    "max_err_over_rms": float(np.abs(o - r).max() / rms)})
     else:
+        if att:
+            dispatch(1)
         for step in range(1, args.steps + 1):
-            box.moe_step(steps[step - 1][0], step, stream)
-            result["steps"].append({"T": steps[step - 1][0]})
+            if att and step < args.steps:
+                dispatch(step + 1)
+            if moe:
+                box.moe_step(steps[step - 1][0], step, stream)
+            if att:
+                combine(step)
         torch.cuda.synchronize()
+    for step in range(1, args.steps + 1):
+        Ts, x, gw, ex = steps[step - 1]
+        if not att:
+            result["steps"].append({"T": Ts})
+            continue
+        first, cnt = plan.shard(Ts, rank)
+        ref = (full.forward_gated(x) if args.gate else full.forward(x, ex, gw))[first:first + cnt]
+        torch.cuda.synchronize()
+        o, r = outs[step].float().cpu().numpy(), ref.float().cpu().numpy()
+        rms = float(np.sqrt(np.mean(r.astype(np.float64) ** 2))) or 1.0
+        bad = int((np.abs(o - r) > RTOL * np.abs(r) + ATOL * rms).sum())
+        result["steps"].append({"T": Ts, "shard": [first, cnt], "bad": bad,
+                                "max_err_over_rms": float(np.abs(o - r).max() / rms)})
     result["timed_out"] = box.timed_out()
     os.makedirs(args.out, exist_ok=True)
-    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}{'g' if args.gate else ''}_rank{rank}.json"), "w") as f:
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}_rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
     dist.destroy_process_group()

@@ -37,7 +37,7 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
     for r in res:
         assert not r["timed_out"], r
         assert r["transport"] == transport
-        if r["role"] == "attention":
+        if r["role"] in ("attention", "both"):
             for s in r["steps"]:
                 assert s["bad"] == 0, s
 
@@ -63,6 +63,29 @@ def test_box_exchange_shared_expert_and_moe_side_gating(flag):
     assert len(res) == attn + moe
     for r in res:
         assert not r["timed_out"], r
-        if r["role"] == "attention":
+        if r["role"] in ("attention", "both"):
             for s_ in r["steps"]:
                 assert s_["bad"] == 0, s_
+
+
+@pytest.mark.parametrize("n,transport", [(2, "nvls"), (4, "nvls"), (4, "p2p")])
+def test_moe_only_colocated_box(n, transport):
+    """The MoE-only box (every rank owns a shard and is an MoE instance), two
+    steps in flight."""
+    if gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29800 + 10 * n + (transport == "p2p")), os.path.join(ROOT, "tests", "dist_worker.py"),
+           "--attn", str(n), "--moe", str(n), "--out", out, "--transport", transport,
+           "--inflight", "2", "--colocated"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
+    assert len(res) == n
+    for r in res:
+        assert not r["timed_out"], r
+        assert r["role"] == "both"
+        for s_ in r["steps"]:
+            assert s_["bad"] == 0, s_
