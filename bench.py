@@ -551,7 +551,10 @@ def run_box(args):
             comb_ms += c0.elapsed_time(c1) / nd
     torch.cuda.synchronize()
     dist.barrier()
-    tvec = torch.tensor([ms, ffn[1], float(launches), disp_ms, moe_ms, comb_ms], device=dev)
+    # the scheduler every MoE GPU runs (replicated, on all T*k slots of the step)
+    sched_us = layer.sched.time_schedule(batches[0], T, K_TOP, reps=51) if layer is not None else 0.0
+    tvec = torch.tensor([ms, ffn[1], float(launches), disp_ms, moe_ms, comb_ms, sched_us],
+                        device=dev)
     allv = [torch.zeros_like(tvec) for _ in range(ws)]
     dist.all_gather(allv, tvec)
     ms_max = max(float(v[0]) for v in allv)
@@ -560,6 +563,7 @@ def run_box(args):
     disp_ms = max(float(v[3]) for v in allv)
     moe_ms = max(float(v[4]) for v in allv)
     comb_ms = max(float(v[5]) for v in allv)
+    sched_us = max(float(v[6]) for v in allv)
 
     # e2e through the host API: attention ranks copy their shard in from pinned
     # host memory and their outputs back each step
@@ -675,6 +679,9 @@ def run_box(args):
             "e2e": {"value": T * args.steps / e2e_s, "unit": "tokens/s",
                     "h2d_bytes_per_step": T * (D_H * 2 + K_TOP * 8),
                     "d2h_bytes_per_step": T * D_H * 2},
+            "scheduler": {"us_per_iter": sched_us, "slots": T * K_TOP,
+                          "how": "CUDA-graph replay of 20 passes on an MoE GPU, median; the "
+                                 "slowest MoE GPU"},
             "gpu_launches": launches_all, "timed_out": timed_out,
             "clocks": clk.summary(),
         }
