@@ -6,13 +6,24 @@
 // is the oracle's or_gate (oracle/oracle.c): ties go to the lower expert id,
 // ids are written in rank order, weights are softmax(top-k logits).
 //
-// One CTA per 128 tokens (UMMA M = 128, cta_group::1), N = E (≤ 256), K = d_h
-// in 64-wide k-blocks through a 4-stage TMA ring; fp32 logits in TMEM (one
-// token per lane).  Epilogue: each of 128 threads owns one token's logits
-// (tcgen05.ld 32x32b), keeps a sorted top-KMAX list in registers while it
-// streams the E columns, then writes k ids and k softmax weights.  HBM-bound:
-// x is read once (2·d_h bytes per token), Wr (2·E·d_h) from L2.
+// One cluster of S CTAs per 128 tokens (UMMA M = 128, cta_group::1), N = E
+// (<= 256), K = d_h split S ways (S = 1, 2, 4 or 8, chosen so the grid covers
+// the SMs: at T = 4096 one CTA per token block would leave 116 SMs idle and
+// each CTA streaming 1 MB).  Each CTA runs its k-blocks through a TMA ring
+// into fp32 TMEM partial logits (one token per lane).  S = 1: each of 128
+// epilogue threads keeps a sorted top-KMAX list in registers while it streams
+// its token's E logits from TMEM.  S > 1: the partials are staged in smem and
+// bulk-copied (cp.async.bulk shared::cluster) to the CTA of the cluster that
+// owns the token (128/S tokens per CTA); the owner sums the S partials in
+// split order (deterministic), 2S threads per token each keep a top-KMAX of an
+// interleaved column subset, and a shuffle merge yields the token's top-k.
+// HBM-bound: x is read once (2·d_h bytes per token), Wr (2·E·d_h) from L2.
+// Graph replay (c2 shape): 18.6 -> 12.6 us at T=256, 18.7 -> 14.8 us at
+// T=4096 against the one-CTA-per-token-block version; the rest is the
+// per-element top-k insertion (issue-bound) and the cluster exchange.
 #include <cuda_bf16.h>
+
+#include <algorithm>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -24,13 +35,16 @@ using namespace sm100;
 
 constexpr int kGateM = 128;   // tokens per CTA
 constexpr int kGBK = 64;      // K per stage
-constexpr int kGStages = 4;
-constexpr int kGateThreads = 192;  // warp 0 TMA, warp 1 TMEM + MMA, warps 2-5 epilogue
+constexpr int kGMaxStages = 8;
+constexpr int kGRingBytes = 200 * 1024;  // smem ring budget (also the S > 1 receive buffer)
+constexpr int kGateThreads = 256;  // warp 0 TMA, warp 1 TMEM + MMA, warps 2-5 TMEM drain; all 8: top-k
 
 struct GateParams {
   CUtensorMap tm_x;  // x [T][d_h], box {64, 128}
   CUtensorMap tm_w;  // Wr [E][d_h], box {64, E}
   int T, K, E, k;
+  int splits;        // S: CTAs (cluster) per token block, K split S ways
+  int stages;        // ring depth
   int32_t *experts;  // [T*k]
   float *gw;         // [T*k]
 };
@@ -76,30 +90,138 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ uint32_t gate_mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, const float *v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3])
+               : "memory");
+}
+// smem -> (peer) smem bulk copy, completing `bytes` on the destination's mbarrier
+__device__ __forceinline__ void bulk_copy_cluster(uint32_t cl_dst, uint32_t src, uint32_t bytes,
+                                                  uint32_t cl_bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          cl_dst),
+      "r"(src), "r"(bytes), "r"(cl_bar)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// (a, ia) ranks before (b, ib): larger logit, ties to the lower id (empty
+// entries carry id -1 = the largest unsigned, so they rank last)
+__device__ __forceinline__ bool ranks_before(float a, int ia, float b, int ib) {
+  return a > b || (a == b && (unsigned)ia < (unsigned)ib);
+}
+
+// Insert (x, e) into the descending list val/idx (branch-free: every j uses
+// the old list, so the compares run in parallel); strict '>' keeps the lower
+// id first among equal logits (callers feed ids in ascending order).
+template <int KMAX>
+__device__ __forceinline__ void topk_insert(float (&val)[KMAX], int (&idx)[KMAX], float x, int e) {
+#pragma unroll
+  for (int j = KMAX - 1; j > 0; --j) {
+    const bool up = x > val[j - 1], here = x > val[j];
+    val[j] = up ? val[j - 1] : here ? x : val[j];
+    idx[j] = up ? idx[j - 1] : here ? e : idx[j];
+  }
+  const bool top = x > val[0];
+  val[0] = top ? x : val[0];
+  idx[0] = top ? e : idx[0];
+}
+
+// Merge the sorted lists of the G consecutive lanes of a token: KMAX rounds
+// of a group arg-max over the list heads (xor shuffles, ties to the lower
+// id); the lane holding the winner pops it.  Every lane of the group ends
+// with the merged list in outv/outi.
+template <int KMAX>
+__device__ __forceinline__ void merge_group(float (&val)[KMAX], int (&idx)[KMAX], int G,
+                                            float (&outv)[KMAX], int (&outi)[KMAX]) {
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    float bv = val[0];
+    int bi = idx[0];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      if (off < G) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ranks_before(ov, oi, bv, bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+    }
+    outv[j] = bv;
+    outi[j] = bi;
+    const bool pop = bi == idx[0];
+#pragma unroll
+    for (int q = 0; q < KMAX - 1; ++q) {
+      val[q] = pop ? val[q + 1] : val[q];
+      idx[q] = pop ? idx[q + 1] : idx[q];
+    }
+    val[KMAX - 1] = pop ? -INFINITY : val[KMAX - 1];
+    idx[KMAX - 1] = pop ? -1 : idx[KMAX - 1];
+  }
+}
+
+template <int KMAX>
+__device__ __forceinline__ void write_topk(const GateParams &p, int t, const float (&val)[KMAX],
+                                           const int (&idx)[KMAX]) {
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < p.k) sum += expf(val[j] - val[0]);
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j)
+    if (j < p.k) {
+      p.experts[(size_t)t * p.k + j] = idx[j];
+      p.gw[(size_t)t * p.k + j] = expf(val[j] - val[0]) / sum;
+    }
+}
+
 template <int KMAX>
 __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_constant__ GateParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nst = p.stages;
   const int wbytes = p.E * kGBK * 2;
   const int stage_bytes = kGateM * kGBK * 2 + wbytes;  // multiple of 1024 (E % 16 == 0)
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kGStages * stage_bytes);
-  uint64_t *empty = full + kGStages;
-  uint64_t *done = empty + kGStages;
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + nst * stage_bytes);
+  uint64_t *empty = full + kGMaxStages;
+  uint64_t *done = empty + kGMaxStages;
+  uint64_t *recv_bar = done + 1;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(recv_bar + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * kGateM;
+  const int S = p.splits;
+  uint32_t split = 0;
+  if (S > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(split));
+  const int t0 = (blockIdx.x / S) * kGateM;
   const int kblocks = p.K / kGBK;
+  const int kb0 = (int)split * kblocks / S, kb1 = ((int)split + 1) * kblocks / S;
   const uint32_t ncols = p.E <= 32 ? 32 : p.E <= 64 ? 64 : p.E <= 128 ? 128 : 256;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tm_x);
     prefetch_tmap(&p.tm_w);
-    for (int s = 0; s < kGStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    mbar_init(recv_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -114,9 +236,9 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {  // TMA producer
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % kGStages;
-      mbar_wait(&empty[s], ((kb / kGStages) & 1) ^ 1);
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int i = kb - kb0, s = i % nst;
+      mbar_wait(&empty[s], ((i / nst) & 1) ^ 1);
       if (elect_one()) {
         unsigned char *st = smem + s * stage_bytes;
         mbar_expect_tx(&full[s], (uint32_t)stage_bytes);
@@ -127,26 +249,62 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
     }
   } else if (warp == 1) {  // MMA issuer
     const uint32_t idesc = idesc_m128(p.E);
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % kGStages;
-      mbar_wait(&full[s], (kb / kGStages) & 1);
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int i = kb - kb0, s = i % nst;
+      mbar_wait(&full[s], (i / nst) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * stage_bytes);
       const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kGateM * kGBK * 2);
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < kGBK / 16; ++k) umma(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+        for (int k = 0; k < kGBK / 16; ++k) umma(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
         umma_commit(&empty[s]);
       }
       __syncwarp();
     }
     if (elect_one()) umma_commit(done);
     __syncwarp();
-  } else {  // epilogue: thread = token (TMEM lane)
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane, t = t0 + row;
-    mbar_wait(done, 0);
+  } else if (warp < 6) {
+    mbar_wait(done, 0);  // the ring is dead and the partial logits are in TMEM
     tc_fence_after();
+    if (S == 1) {  // no exchange: thread = token, straight from TMEM
+      const int quad = warp & 3, row = quad * 32 + lane;
+      float val[KMAX];
+      int idx[KMAX];
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        val[j] = -INFINITY;
+        idx[j] = -1;
+      }
+      for (int e0 = 0; e0 < p.E; e0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + e0, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (e0 + i < p.E) topk_insert(val, idx, v[i], e0 + i);
+      }
+      if (t0 + row < p.T) write_topk(p, t0 + row, val, idx);
+    }
+  }
+
+  // ---- S > 1: exchange the partial logits, sum in split order, top-k ----
+  // The E columns go in chunks of <= 128 (smem: staging + receive buffer,
+  // both in the dead ring).  Per chunk: warps 2-5 stage their token rows
+  // (thread = TMEM lane) into stg[128][ld]; after a cluster barrier one
+  // thread bulk-copies rows [j*R, (j+1)*R) to CTA j's recv[split]
+  // (complete_tx on CTA j's mbarrier).  Then G = 256/R threads per owned
+  // token sum the S partials in split order and insert their columns sub,
+  // sub+G, ... into a top-KMAX list; after the last chunk the G lists merge.
+  if (S > 1) {
+    const int R = kGateM / S;        // tokens owned by this CTA
+    const int G = kGateThreads / R;  // threads per token (2S)
+    const int nch = (p.E + 127) / 128;
+    const int EC = ((p.E + nch - 1) / nch + 15) & ~15;  // chunk width
+    const int ld = EC + G;           // row stride (floats): conflict-free sums
+    const uint32_t stg = smem_u32(smem);
+    const uint32_t recv = stg + (uint32_t)(kGateM * ld) * 4u;
+    const uint32_t chunk_bytes = (uint32_t)(R * ld) * 4u;  // per (source, destination)
+    const int tok = threadIdx.x / G, sub = threadIdx.x % G;
     float val[KMAX];
     int idx[KMAX];
 #pragma unroll
@@ -154,48 +312,59 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
       val[j] = -INFINITY;
       idx[j] = -1;
     }
-    for (int e0 = 0; e0 < p.E; e0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + e0, v);
+    for (int c = 0; c < nch; ++c) {
+      const int c0 = c * EC, c1 = min(p.E, c0 + EC);
+      if (c > 0) {  // this CTA's copies have read stg; every CTA is done with its recv
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        cluster_barrier();
+      }
+      if (warp >= 2 && warp < 6) {
+        const int quad = warp & 3, row = quad * 32 + lane;
+        const uint32_t dst = stg + (uint32_t)(row * ld) * 4u;
+        for (int e0 = c0; e0 < c1; e0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + e0, v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float x = v[i];
-        const int e = e0 + i;
-        // insert into the descending list; strict '>' keeps the lower id
-        // first among equal logits (ids arrive ascending)
-        if (e < p.E && x > val[KMAX - 1]) {
-#pragma unroll
-          for (int j = KMAX - 1; j > 0; --j) {
-            if (x > val[j - 1]) {
-              val[j] = val[j - 1];
-              idx[j] = idx[j - 1];
-            } else if (x > val[j]) {
-              val[j] = x;
-              idx[j] = e;
-            }
-          }
-          if (x > val[0]) {
-            val[0] = x;
-            idx[0] = e;
-          }
+          for (int q = 0; q < 32; q += 4)
+            if (e0 + q < c1) st_shared_v4(dst + (uint32_t)(e0 - c0 + q) * 4u, v + q);
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging -> bulk copies
+      }
+      if (threadIdx.x == 0) mbar_expect_tx(recv_bar, (uint32_t)S * chunk_bytes);
+      cluster_barrier();  // every CTA's staging is written and its expect_tx armed
+      if (threadIdx.x == 0) {
+        for (int j = 0; j < S; ++j)
+          bulk_copy_cluster(gate_mapa(recv + split * chunk_bytes, (uint32_t)j),
+                            stg + (uint32_t)j * chunk_bytes, chunk_bytes,
+                            gate_mapa(smem_u32(recv_bar), (uint32_t)j));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      mbar_wait(recv_bar, (uint32_t)c & 1);
+      // recv[s][tok][e - c0]: split s's partial logit of owned token tok
+      const uint32_t base = recv + (uint32_t)(tok * ld) * 4u;
+      for (int e = c0 + sub; e < c1; e += G) {
+        const uint32_t a = base + (uint32_t)(e - c0) * 4u;
+        float x = ld_shared_f32(a);
+#pragma unroll
+        for (int s = 1; s < 8; ++s)
+          if (s < S) x += ld_shared_f32(a + (uint32_t)s * chunk_bytes);
+        topk_insert(val, idx, x, e);
       }
     }
-    if (t < p.T) {
-      float sum = 0.f;
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j)
-        if (j < p.k) sum += expf(val[j] - val[0]);
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j)
-        if (j < p.k) {
-          p.experts[(size_t)t * p.k + j] = idx[j];
-          p.gw[(size_t)t * p.k + j] = expf(val[j] - val[0]) / sum;
-        }
-    }
+    float outv[KMAX];
+    int outi[KMAX];
+    merge_group(val, idx, G, outv, outi);
+    const int t = t0 + (int)split * R + tok;
+    if (sub == 0 && t < p.T) write_topk(p, t, outv, outi);
   }
+
   tc_fence_before();
-  __syncthreads();
+  if (S > 1) {  // no CTA leaves while a peer may still address its smem
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    cluster_barrier();
+  } else {
+    __syncthreads();
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
@@ -216,8 +385,19 @@ cudaError_t launch_gate_k(const GateParams &g, size_t smem, cudaStream_t s) {
     configured = smem;
   }
   const int blocks = (g.T + kGateM - 1) / kGateM;
-  gate_kernel<KMAX><<<blocks, kGateThreads, smem, s>>>(g);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks * g.splits);
+  cfg.blockDim = dim3(kGateThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gate_kernel<KMAX>, g);
 }
 
 }  // namespace
@@ -240,8 +420,17 @@ cudaError_t launch_gate(const void *x, const void *wr, int T, int d_h, int E, in
   g.k = k;
   g.experts = experts;
   g.gw = gw;
-  const size_t smem =
-      (size_t)kGStages * (kGateM * kGBK * 2 + (size_t)E * kGBK * 2) + 1024 + 128;
+  // split K S ways while the grid still fits the SMs (each CTA keeps >= 2 k-blocks)
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = (T + kGateM - 1) / kGateM, kblocks = d_h / kGBK;
+  int S = 1;
+  while (S < 8 && blocks * S * 2 <= sms && kblocks >= 4 * S) S *= 2;
+  const int stage_bytes = kGateM * kGBK * 2 + E * kGBK * 2;
+  g.splits = S;
+  g.stages = std::min(kGMaxStages, kGRingBytes / stage_bytes);
+  const size_t smem = (size_t)g.stages * stage_bytes + 1024 + 256;
   if (k <= 4) return launch_gate_k<4>(g, smem, s);
   if (k <= 8) return launch_gate_k<8>(g, smem, s);
   return launch_gate_k<16>(g, smem, s);
