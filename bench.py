@@ -459,6 +459,9 @@ def run_box(args):
         rmap, _ = shape_map(J, M)
         layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
+        if args.gate:  # MoE-side gating: this GPU routes the rows itself
+            from paper_2512_13525_b200.moe import router_weights
+            layer.set_router(router_weights(E, D_H, 13, dev))
     box = JanusBox(plan, rank, T, D_H, K_TOP, layer=layer, device=local,
                    transport=args.transport)
     pat = J.RoutingPattern.zipf(E, 1.0)
@@ -469,6 +472,9 @@ def run_box(args):
     xs = x[first:first + cnt].contiguous()
     gws = [gw[first * K_TOP:(first + cnt) * K_TOP].contiguous()] if att else []
     exs = [b[first * K_TOP:(first + cnt) * K_TOP].contiguous() for b in batches]
+    if args.gate:  # the attention GPUs ship rows only
+        gws = [None] if att else []
+        exs = [None] * N_BATCHES
     out = torch.empty(max(cnt, 1), D_H, dtype=torch.bfloat16, device=dev)
     s = torch.cuda.current_stream(dev)
     stream = s.cuda_stream
@@ -569,10 +575,12 @@ def run_box(args):
     # host memory and their outputs back each step
     if att:
         xh = xs.cpu().pin_memory()
-        exh = [e.cpu().pin_memory() for e in exs]
-        gwh = gws[0].cpu().pin_memory()
         oh = torch.empty(max(cnt, 1), D_H, dtype=torch.bfloat16).pin_memory()
-        xd, exd, gwd = torch.empty_like(xs), torch.empty_like(exs[0]), torch.empty_like(gws[0])
+        xd = torch.empty_like(xs)
+        if not args.gate:
+            exh = [e.cpu().pin_memory() for e in exs]
+            gwh = gws[0].cpu().pin_memory()
+            exd, gwd = torch.empty_like(exs[0]), torch.empty_like(gws[0])
     dist.barrier()
     t0 = time.perf_counter()
     e0_ = epoch[0]
@@ -581,8 +589,8 @@ def run_box(args):
         # combine i (compute stream), D2H of step i's output (second copy
         # stream) — every step's bytes cross PCIe, overlapped with the layer
         xd2 = [xd, torch.empty_like(xd)]
-        exd2 = [exd, torch.empty_like(exd)]
-        gwd2 = [gwd, torch.empty_like(gwd)]
+        exd2 = [exd, torch.empty_like(exd)] if not args.gate else [None, None]
+        gwd2 = [gwd, torch.empty_like(gwd)] if not args.gate else [None, None]
         out2 = [out, torch.empty_like(out)]
         h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ev_in = [torch.cuda.Event(), torch.cuda.Event()]    # inputs of slot b landed
@@ -596,8 +604,9 @@ def run_box(args):
                 if i >= 2:
                     h2d_s.wait_event(ev_used[b])
                 xd2[b].copy_(xh, non_blocking=True)
-                exd2[b].copy_(exh[i % N_BATCHES], non_blocking=True)
-                gwd2[b].copy_(gwh, non_blocking=True)
+                if not args.gate:
+                    exd2[b].copy_(exh[i % N_BATCHES], non_blocking=True)
+                    gwd2[b].copy_(gwh, non_blocking=True)
                 ev_in[b].record(h2d_s)
             s.wait_event(ev_in[b])
             box.dispatch(xd2[b], exd2[b], gwd2[b], T, e0_ + i + 1, stream)
@@ -632,7 +641,7 @@ def run_box(args):
     timed_out = box.timed_out()
     if rank == 0:
         value = T * args.steps / (ms_max / 1e3)
-        sends = plan.bytes_per_step(T, D_H, K_TOP)
+        sends = plan.bytes_per_step(T, D_H, 0 if args.gate else K_TOP)
         send_bytes = sends[0][0]
         hbm, tf_burst, tf_sus, src = peaks()
         line = {
@@ -654,6 +663,10 @@ def run_box(args):
                        "tokens_per_step": T, "tokens_per_moe_gpu": args.tokens,
                        "replica_map": shape_map_name(M),
                        "parallelism": f"{M} x (A+E)" if plan.colocated else f"{A}A+{M}E",
+                       "gating": "MoE-side: rows only cross NVLink, every MoE GPU runs "
+                                 "gate_kernel on the full step" if args.gate else
+                                 "attention-side: top-k ids and gate weights shipped with "
+                                 "the rows",
                        "l2": "inputs > L2 (weights streamed)"},
             "tokens_per_s_per_gpu": value / ws, "tokens_per_s_per_moe_gpu": value / M,
             "roofline": {"bound": "hbm", "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
@@ -677,7 +690,7 @@ def run_box(args):
                        "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy "
                                                          "per direction (fallback)"},
             "e2e": {"value": T * args.steps / e2e_s, "unit": "tokens/s",
-                    "h2d_bytes_per_step": T * (D_H * 2 + K_TOP * 8),
+                    "h2d_bytes_per_step": T * (D_H * 2 + (0 if args.gate else K_TOP * 8)),
                     "d2h_bytes_per_step": T * D_H * 2},
             "scheduler": {"us_per_iter": sched_us, "slots": T * K_TOP,
                           "how": "CUDA-graph replay of 20 passes on an MoE GPU, median; the "
@@ -704,6 +717,9 @@ def main():
                          "4), or the MoE-only box (every GPU owns tokens and experts)")
     ap.add_argument("--shape", default="c2", choices=sorted(SHAPES),
                     help="expert shape (BASELINE configs); c2 is the headline")
+    ap.add_argument("--gate", action="store_true",
+                    help="box: MoE-side gating (rows only cross NVLink; every MoE GPU runs "
+                         "the router GEMM + top-k on the full step)")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls"],
                     help="box exchange for --gpus > 1 (auto: NVLS multicast when supported)")
     args = ap.parse_args()
