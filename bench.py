@@ -69,12 +69,14 @@ def shape_map(J, M):
     return J.config_map(f"c4_n{M}"), f"c4_n{M}"
 
 
-def set_shared_expert(layer, dev):
-    if SHARED and layer.instance <= 0:
+def set_shared_expert(layer, dev, split=False):
+    """split (box): every MoE instance runs the shared expert on its even share
+    of the tokens (janus_moe_set_shared_split) instead of instance 0 on all."""
+    if SHARED and (split or layer.instance <= 0):
         import torch
         from paper_2512_13525_b200.moe import expert_weights
         wg, wu, wd = expert_weights(E, D_H, D_E, 1, dev)
-        layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
+        layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous(), split=split)
 
 
 def peaks():
@@ -459,6 +461,7 @@ def run_box(args):
         rmap, _ = shape_map(J, M)
         layer = MoELayer(rmap, D_H, D_E, T, K_TOP, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
+        set_shared_expert(layer, dev, split=True)  # DS-V3 shape: shared expert split over instances
         if args.gate:  # MoE-side gating: this GPU routes the rows itself
             from paper_2512_13525_b200.moe import router_weights
             layer.set_router(router_weights(E, D_H, 13, dev))
@@ -661,6 +664,8 @@ def run_box(args):
                                                      else "peer-memory (P2P) kernels"),
                        "transport": box.transport,
                        "tokens_per_step": T, "tokens_per_moe_gpu": args.tokens,
+                       "shared_expert": "every MoE GPU on its even share of the tokens"
+                                        if SHARED else False,
                        "replica_map": shape_map_name(M),
                        "parallelism": f"{M} x (A+E)" if plan.colocated else f"{A}A+{M}E",
                        "gating": "MoE-side: rows only cross NVLink, every MoE GPU runs "

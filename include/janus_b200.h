@@ -132,6 +132,12 @@ janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *d_w
  * w2 [d_h][d_e], bf16, caller-owned; NULL disables.  Computed by the
  * single-GPU layer, and by MoE instance 0 of a box (NVLS transport). */
 janus_status janus_moe_set_shared(janus_ctx *ctx, const void *d_w13, const void *d_w2);
+/* Shared expert placement in a box: 0 (default) = MoE instance 0 runs it on
+ * every token; 1 = every MoE instance runs it on an even share of the step's
+ * tokens (instance g of N: [g*(T/N) + min(g, T%N), +T/N + (g < T%N)) — the
+ * same split as the attention shards), so no instance straggles by a dense
+ * FFN over the whole step.  Set the weights on every MoE instance for 1. */
+janus_status janus_moe_set_shared_split(janus_ctx *ctx, int split);
 janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                                    const float *d_gate_w, int num_tokens, void *d_out,
                                    const janus_assignment *assign, void *stream);

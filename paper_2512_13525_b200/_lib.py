@@ -31,6 +31,7 @@ SYMBOLS = (
     "janus_moe_set_router", "janus_moe_layer_gated_async", "janus_stats_configure",
     "janus_stats_record_async", "janus_stats_read", "janus_stats_status",
     "janus_moe_layer_host_async", "janus_moe_host_sync", "janus_moe_set_shared",
+    "janus_moe_set_shared_split",
     "janus_xfer_configure_colocated",
 )
 
@@ -95,6 +96,7 @@ def _load() -> C.CDLL:
     L.janus_moe_layer_host_async.argtypes = [vp, vp, vp, vp, i32, vp]
     L.janus_moe_host_sync.argtypes = [vp]
     L.janus_moe_set_shared.argtypes = [vp, vp, vp]
+    L.janus_moe_set_shared_split.argtypes = [vp, i32]
     L.janus_xfer_configure_colocated.argtypes = [vp, i32, i32, i32, i32, i32]
     return L
 

@@ -407,12 +407,12 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
       for (int q = tid; q <= R; q += kSchedThreads) a.out.group_off[q] = qcnt[q];
     if (a.tile_off)
       for (int q = tid; q <= R; q += kSchedThreads) a.tile_off[q] = tcnt[q];
-    if (a.shared_off && tid == 0) {  // one group of every token, token order
-      const int T = a.S / a.k;
+    if (a.shared_off && tid == 0) {  // one group of this instance's shared tokens
+      const int rows = a.shared_rows;
       a.shared_off[0] = 0;
-      a.shared_off[1] = T;
+      a.shared_off[1] = rows;
       a.shared_off[2] = 0;
-      a.shared_off[3] = T > 0 ? (T + a.shared_tile_n - 1) / a.shared_tile_n : 0;
+      a.shared_off[3] = rows > 0 ? (rows + a.shared_tile_n - 1) / a.shared_tile_n : 0;
     }
     for (int g = tid; g < N; g += kSchedThreads) {
       a.out.load[g] = load[g];

@@ -274,7 +274,8 @@ janus_status janus_replica_order(const janus_ctx *ctx, int32_t *qidx, int32_t *q
 static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T, int k,
                                  int policy, uint64_t seed, const janus_assignment &out,
                                  int32_t *tile_off, cudaStream_t stream,
-                                 int32_t *shared_off = nullptr, int shared_tile_n = 0) {
+                                 int32_t *shared_off = nullptr, int shared_tile_n = 0,
+                                 int shared_rows = 0) {
   if (T < 0 || k <= 0 || (int64_t)T * k > (int64_t)1 << 30)
     return fail(ctx, JANUS_EINVAL, "batch: num_tokens must be >= 0 and top_k >= 1");
   if (policy != JANUS_POLICY_AEBS && policy != JANUS_POLICY_RANDOM)
@@ -299,6 +300,7 @@ static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T
   a.merge_tail = a.tile_n <= 64;
   a.shared_off = shared_off;
   a.shared_tile_n = shared_tile_n;
+  a.shared_rows = shared_rows;
   cudaError_t e = janus::launch_schedule(a, stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aebs_schedule_kernel");
   ctx->launches += 1;
@@ -516,6 +518,15 @@ janus_status janus_moe_set_shared(janus_ctx *ctx, const void *w13, const void *w
   return JANUS_OK;
 }
 
+janus_status janus_moe_set_shared_split(janus_ctx *ctx, int split) {
+  janus_status st = check_ready(ctx);
+  if (st != JANUS_OK) return st;
+  if (split != 0 && split != 1) return fail(ctx, JANUS_EINVAL, "moe: shared split must be 0 or 1");
+  clear_graphs(ctx);
+  ctx->shared_split = split;
+  return JANUS_OK;
+}
+
 janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *w13, const void *w2) {
   janus_status st = check_ready(ctx);
   if (st != JANUS_OK) return st;
@@ -580,18 +591,30 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     CK(cudaEventRecord(ev[0], s));
   }
   janus::sm100::pdl_enabled = ev == nullptr;  // events between PDL kernels would mis-time them
-  // the shared expert (every token) runs on the single-GPU layer, and on MoE
-  // instance 0 of a box (its partial sums carry it)
-  const bool shared = ctx->shared && ctx->instance <= 0;
+  // the shared expert (every token) runs on the single-GPU layer; in a box
+  // on MoE instance 0 (its partial sums carry it), or with shared_split on
+  // every MoE instance for an even share of the tokens (remainder to the low
+  // instances), so no instance straggles by a dense FFN over the whole step
+  int sh0 = 0, sh1 = 0;
+  if (ctx->shared) {
+    if (ctx->instance < 0 || (!ctx->shared_split && ctx->instance == 0)) {
+      sh1 = T;
+    } else if (ctx->shared_split) {
+      const int n = ctx->dmap.N, g = ctx->instance, base = T / n, rem = T % n;
+      sh0 = g * base + std::min(g, rem);
+      sh1 = sh0 + base + (g < rem ? 1 : 0);
+    }
+  }
+  const bool shared = sh1 > sh0;
   janus::FfnPlan &ps = ctx->ffn_shared;
-  if (shared) ps.tile_n = T <= 64 ? 64 : janus::kTileN;
+  if (shared) ps.tile_n = sh1 - sh0 <= 64 ? 64 : janus::kTileN;
   st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, ctx->ws_tile_off, s,
-                    shared ? ctx->shared_off : nullptr, shared ? ps.tile_n : 0);
+                    shared ? ctx->shared_off : nullptr, shared ? ps.tile_n : 0, sh1 - sh0);
   if (st != JANUS_OK) return st;
   if (ev) CK(cudaEventRecord(ev[1], s));
   janus::FfnPlan &p = ctx->ffn;
   cudaError_t e = janus::launch_permute(d_x, a.slot_row, a.instance, ctx->instance, T * k, k,
-                                        p.d_h, p.xp, shared ? ps.xp : nullptr, s);
+                                        p.d_h, p.xp, shared ? ps.xp : nullptr, sh0, sh1, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "permute_kernel");
   int launches = 0;
   if (ev) CK(cudaEventRecord(ev[2], s));
@@ -607,7 +630,7 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
                               reinterpret_cast<void *>(x.uc_va + x.mpart_off +
                                                        janus::xfer_slot(push_epoch) * x.mslot),
-                              s, shared ? ps.y : nullptr);
+                              s, shared ? ps.y : nullptr, sh0, sh1);
     if (e == cudaSuccess) e = janus::launch_signal_combine(x, push_epoch, s);
     launches += 1;
   } else if (push_epoch) {
@@ -616,7 +639,7 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
                                    push_epoch, s);
   } else
     e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
-                              d_out, s, shared ? ps.y : nullptr);
+                              d_out, s, shared ? ps.y : nullptr, sh0, sh1);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
   ctx->launches += 2 + launches;  // permute, combine, GEMMs (launch_sched counts itself)
   return JANUS_OK;

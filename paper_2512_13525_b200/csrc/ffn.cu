@@ -35,7 +35,8 @@ constexpr int kWarpsPerBlock = 4;
 
 __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__restrict__ slot_row,
                                const int32_t *__restrict__ slot_inst, int instance, int T, int k,
-                               int vec, uint4 *__restrict__ xp, uint4 *__restrict__ xp_shared) {
+                               int vec, uint4 *__restrict__ xp, uint4 *__restrict__ xp_shared,
+                               int sh0, int sh1) {
   sm100::pdl_trigger();
   sm100::pdl_wait();  // slot_row / slot_inst from K1
   const int lane = threadIdx.x & 31;
@@ -46,13 +47,13 @@ __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__res
   const uint4 *src = x + (size_t)t * vec;
   uint4 v[kPermU];
   bool loaded = false;  // x is read only if some slot of t is routed here
-  if (xp_shared) {      // the shared expert takes every token, in token order
+  if (xp_shared && t >= sh0 && t < sh1) {  // the shared expert's tokens, in token order
 #pragma unroll
     for (int u = 0; u < kPermU; ++u) {
       const int c = c0 + 32 * u;
       if (c < vec) {
         v[u] = __ldg(src + c);
-        xp_shared[(size_t)t * vec + c] = v[u];
+        xp_shared[(size_t)(t - sh0) * vec + c] = v[u];
       }
     }
     loaded = true;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
     combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
                    const int32_t *__restrict__ slot_inst, int instance,
                    const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out,
-                   const uint4 *__restrict__ y_shared) {
+                   const uint4 *__restrict__ y_shared, int sh0, int sh1) {
   sm100::pdl_trigger();
   sm100::pdl_wait();  // y from the down GEMM
   const int lane = threadIdx.x & 31;
@@ -168,12 +169,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
         }
     }
   }
-  if (y_shared) {  // the shared expert, weight 1, after the routed slots
+  if (y_shared && t >= sh0 && t < sh1) {  // the shared expert, weight 1, after the routed slots
 #pragma unroll
     for (int u = 0; u < kCombU; ++u) {
       const int c = c0 + 32 * u;
       if (c >= vec) continue;
-      const uint4 v = __ldg(y_shared + (size_t)t * vec + c);
+      const uint4 v = __ldg(y_shared + (size_t)(t - sh0) * vec + c);
       const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
 
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, int S, int k, int d_h, void *xp, void *xp_shared,
-                           cudaStream_t s) {
+                           int sh0, int sh1, cudaStream_t s) {
   if (S == 0) return cudaSuccess;
   const int T = S / k, vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kPermU - 1) / (32 * kPermU));
@@ -207,12 +208,12 @@ cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t
   return sm100::launch_pdl(permute_kernel, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
                            reinterpret_cast<const uint4 *>(x), slot_row, slot_instance, instance,
                            T, k, vec, reinterpret_cast<uint4 *>(xp),
-                           reinterpret_cast<uint4 *>(xp_shared));
+                           reinterpret_cast<uint4 *>(xp_shared), sh0, sh1);
 }
 
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
-                           cudaStream_t s, const void *y_shared) {
+                           cudaStream_t s, const void *y_shared, int sh0, int sh1) {
   if (T == 0) return cudaSuccess;
   const int vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kCombU - 1) / (32 * kCombU));
@@ -220,7 +221,7 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
   return sm100::launch_pdl(combine_kernel<4>, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
                            reinterpret_cast<const uint4 *>(y), slot_row, slot_instance, instance,
                            gate_w, T, k, vec, reinterpret_cast<uint4 *>(out),
-                           reinterpret_cast<const uint4 *>(y_shared));
+                           reinterpret_cast<const uint4 *>(y_shared), sh0, sh1);
 }
 
 }  // namespace janus

@@ -33,8 +33,9 @@ struct SchedArgs {
   uint64_t *trace;     // [7] phase timestamps (%globaltimer), optional
   int id_bits;         // bits of the largest expert id (ballot-based peer matching)
   int merge_tail;      // 1: a group's last n-tile also takes the remainder (wide tiles)
-  int32_t *shared_off;  // optional [4]: the shared expert's {0, T} rows and {0, n-tiles}
+  int32_t *shared_off;  // optional [4]: the shared expert's {0, rows} and {0, n-tiles}
   int shared_tile_n;
+  int shared_rows;      // tokens this instance runs the shared expert on
 };
 
 inline int id_bits_for(int E) {
@@ -64,18 +65,21 @@ struct FfnPlan {
 };
 
 cudaError_t build_ffn_tensor_maps(FfnPlan &p);
-// xp_shared (optional): also store row t of x at xp_shared[t] (the shared
-// expert's token rows, in token order)
+// xp_shared (optional): also store row t of x at xp_shared[t - sh0] for
+// t in [sh0, sh1) (the shared expert's token rows, in token order)
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, int S, int k, int d_h, void *xp, void *xp_shared,
+                           int sh0, int sh1,
                            cudaStream_t s);
 // gate/up GEMM with fused SwiGLU, then the down GEMM; 2 launches.
 cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
                        cudaStream_t s, int *launches);
-// y_shared (optional): + y_shared[t] (weight 1) after the k routed slots
+// y_shared (optional): + y_shared[t - sh0] (weight 1) after the k routed
+// slots, for t in [sh0, sh1)
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
-                           cudaStream_t s, const void *y_shared = nullptr);
+                           cudaStream_t s, const void *y_shared = nullptr, int sh0 = 0,
+                           int sh1 = 0);
 
 // MoE-side gating (gate.cu): router GEMM + top-k + softmax of the top-k logits.
 bool gate_shape_ok(int d_h, int E, int k);
@@ -177,7 +181,8 @@ struct janus_ctx {
   // every token, its own GEMM plan over token-ordered rows that K3 also writes
   bool shared = false;
   janus::FfnPlan ffn_shared;
-  int32_t *shared_off = nullptr;  // [4] {0, T} rows, {0, n-tiles}
+  int32_t *shared_off = nullptr;  // [4] {0, rows}, {0, n-tiles}
+  int shared_split = 0;  // 1: every MoE instance takes an even share of the tokens
   janus_assignment ws{};      // device workspace for the layer's assignment
   int32_t *ws_tile_off = nullptr;
   // staging for the host MoE API

@@ -143,9 +143,12 @@ class MoELayer:
             raise JanusError(st, self.sched.last_error())
         return out
 
-    def set_shared(self, w13: torch.Tensor | None, w2: torch.Tensor | None = None) -> None:
+    def set_shared(self, w13: torch.Tensor | None, w2: torch.Tensor | None = None,
+                   split: bool = False) -> None:
         """DeepSeek-V3-style shared expert on every token (weight 1):
-        w13 [2*d_e][d_h] = [Wg; Wu], w2 [d_h][d_e] bf16; None disables."""
+        w13 [2*d_e][d_h] = [Wg; Wu], w2 [d_h][d_e] bf16; None disables.
+        split (box MoE instances): every instance takes an even share of the
+        tokens instead of instance 0 taking all (janus_moe_set_shared_split)."""
         if w13 is None:
             self.shared_w = None
             st = lib.janus_moe_set_shared(self.ctx, None, None)
@@ -155,6 +158,8 @@ class MoELayer:
             assert w2.is_contiguous() and w13.is_cuda and w2.is_cuda
             self.shared_w = (w13, w2)  # keep alive: the context stores raw pointers
             st = lib.janus_moe_set_shared(self.ctx, w13.data_ptr(), w2.data_ptr())
+        if st == OK:
+            st = lib.janus_moe_set_shared_split(self.ctx, 1 if split else 0)
         if st != OK:
             raise JanusError(st, self.sched.last_error())
 

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--out", default="gpurun_out")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls"])
     ap.add_argument("--shared", action="store_true", help="add a shared expert (NVLS only)")
+    ap.add_argument("--shared-split", action="store_true",
+                    help="the shared expert split evenly over the MoE instances (implies --shared)")
     ap.add_argument("--colocated", action="store_true",
                     help="MoE-only box: every rank owns a shard and is an MoE instance")
     ap.add_argument("--gate", action="store_true",
@@ -56,12 +58,13 @@ def main():
     if moe:
         layer = MoELayer(rmap, d_h, d_e, T, k, instance=plan.instance(rank), device=local)
         layer.set_weights(*build_weight_store(layer, seed=1))
+    args.shared = args.shared or args.shared_split
     if args.shared:
         from paper_2512_13525_b200.moe import expert_weights
         wg, wu, wd = expert_weights(99, d_h, d_e, 5, dev)
         shared_w = (torch.cat([wg, wu]).contiguous(), wd.contiguous())
         if layer is not None:
-            layer.set_shared(*shared_w)
+            layer.set_shared(*shared_w, split=args.shared_split)
     if args.gate:
         from paper_2512_13525_b200.moe import router_weights
         wr = router_weights(E, d_h, 13, dev)
@@ -142,7 +145,7 @@ def main():
                                 "max_err_over_rms": float(np.abs(o - r).max() / rms)})
     result["timed_out"] = box.timed_out()
     os.makedirs(args.out, exist_ok=True)
-    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}_rank{rank}.json"), "w") as f:
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}{'x' if args.shared_split else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}_rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
     dist.destroy_process_group()

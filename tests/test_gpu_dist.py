@@ -42,10 +42,11 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
                 assert s["bad"] == 0, s
 
 
-@pytest.mark.parametrize("flag", ["--shared", "--gate"])
+@pytest.mark.parametrize("flag", ["--shared", "--shared-split", "--gate"])
 def test_box_exchange_shared_expert_and_moe_side_gating(flag):
     """--shared: the shared expert in a box (MoE instance 0 adds it to its
-    partials).  --gate: rows only are dispatched and every MoE rank computes
+    partials); --shared-split: every MoE instance adds it for its share of the
+    tokens.  --gate: rows only are dispatched and every MoE rank computes
     the routing with the gating kernel (Janus gates on the MoE side).  NVLS
     transport, two steps in flight."""
     attn, moe = 1, 3
@@ -54,7 +55,7 @@ def test_box_exchange_shared_expert_and_moe_side_gating(flag):
     out = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={attn + moe}", "--master-addr", "127.0.0.1", "--master-port",
-           str(29777 + (flag == "--gate")), os.path.join(ROOT, "tests", "dist_worker.py"),
+           str(29777 + ["--shared", "--shared-split", "--gate"].index(flag)), os.path.join(ROOT, "tests", "dist_worker.py"),
            "--attn", str(attn), "--moe",
            str(moe), "--out", out, "--transport", "nvls", "--inflight", "2", flag]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
