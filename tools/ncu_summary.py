@@ -11,6 +11,7 @@ import sys
 
 KEYS = [
     ("gpu__time_duration.sum", "duration"),
+    ("smsp__cycles_elapsed.avg.per_second", "sm_clock"),
     ("dram__bytes_read.sum", "dram_read"),
     ("dram__bytes_write.sum", "dram_write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"),
