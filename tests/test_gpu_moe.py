@@ -156,6 +156,21 @@ def test_qwen3_30b_shape_sampled_tokens(J, oracle):
     check_close(bf16_to_f32(u16(out))[tokens], ref, "c2 T=256")
 
 
+@pytest.mark.parametrize("T", [4096, 4099])
+def test_qwen3_30b_bench_size_sampled_tokens(J, oracle, T):
+    """The bench workload at full size (c2 map, Zipf 1.0, T=4096: the
+    tensor-regime tiles of 256 token rows) and a ragged step just above it:
+    sampled tokens vs the fp32 oracle, the first and last tokens included."""
+    rm = J.config_map("c2")
+    layer = make_layer(J, rm, 2048, 768, T, 8)
+    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, 8, 0x30, T * 1000)
+    x, ex, gw, out = run(J, layer, b.experts, T)
+    tokens = np.concatenate([[0, T - 1], np.random.default_rng(T).choice(
+        np.arange(1, T - 1), 46, replace=False)])
+    ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens)
+    check_close(bf16_to_f32(u16(out))[tokens], ref, f"c2 T={T}")
+
+
 def test_layer_assignment_bit_exact_and_host_e2e(J, oracle):
     import torch
     from paper_maps import load_map_csr
