@@ -24,6 +24,7 @@ PATTERNS = {
     "c1_uniform": (lambda: J.RoutingPattern.uniform(64), 0x5EED),
     "c1_gaussian": (lambda: J.RoutingPattern.gaussian(64, 0.15), 0x5EED),
     "c2": (lambda: J.RoutingPattern.zipf(128, 1.0), 0x30),
+    "c2_m3": (lambda: J.RoutingPattern.zipf(128, 1.0), 0x30),
     "c3": (lambda: J.RoutingPattern.zipf(128, 1.0), 0x235),
     "c4_n2": (lambda: J.RoutingPattern.zipf(256, 1.0), 0xD5),
     "c4_n4": (lambda: J.RoutingPattern.zipf(256, 1.0), 0xD5),
