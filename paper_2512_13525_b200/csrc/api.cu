@@ -576,8 +576,10 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     a.status = assign->status ? assign->status : a.status;
   }
   // GEMM n-tile: decode steps (few rows per replica group) use 64-row tiles
-  // and the deep 9-stage weight ring; larger steps 256-row tiles
-  ctx->ffn.tile_n = (int64_t)T * k <= 48LL * ctx->dmap.E ? 64 : janus::kTileN;
+  // and the deep 9-stage weight ring; larger steps 256-row tiles.
+  // Crossover measured on the c2 shape (FFN µs, 64 vs 256-row tiles): 24 rows
+  // per expert 194.5 vs 196.0, 32: 204.2 vs 200.9, 48: 218.5 vs 209.2.
+  ctx->ffn.tile_n = (int64_t)T * k <= 28LL * ctx->dmap.E ? 64 : janus::kTileN;
   cudaEvent_t *ev = nullptr;
   if (ctx->profiling) {
     const size_t need = 4 * (size_t)(ctx->prof_calls + 1);
