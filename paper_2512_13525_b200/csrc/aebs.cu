@@ -32,6 +32,7 @@
 // multi-replica expert (~40 cycles each).
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <climits>
 
 #include "internal.h"
@@ -502,10 +503,13 @@ size_t schedule_smem_bytes(int E, int N, int R) {
 }
 
 int schedule_cluster_size(int S) {
-  // aim at <= 2048 slots (2 windows per warp) per CTA; above 8 CTAs (S > 16 K
-  // slots, e.g. the box path's MoE GPUs scheduling every attention shard) the
-  // cluster grows to 16
-  int c = (S + 2047) / 2048;
+  // ~1024 slots per CTA, and at least 4 CTAs once there are 512 per CTA; the
+  // per-phase cost is mostly barrier latency, so small steps gain from more
+  // CTAs only up to a point (graph-replayed µs, tools/sched_sweep.py, c2 map:
+  // 2048 slots 9.3 / 8.4 / 8.0 / 8.1 µs on 1 / 2 / 4 / 8 CTAs; 6144 slots
+  // 9.8 / 8.9 / 9.4 / 9.9 on 3 / 6 / 12 / 16).  Above 16 K slots (the box
+  // path's MoE GPUs scheduling every attention shard) the cluster is 16.
+  const int c = std::max((S + 1023) / 1024, std::min(4, (S + 511) / 512));
   return c < 1 ? 1 : (c > kMaxCluster ? kMaxCluster : c);
 }
 
