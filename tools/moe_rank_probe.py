@@ -19,6 +19,7 @@ ap.add_argument("--moe", type=int, default=3)
 ap.add_argument("--tokens-per-gpu", type=int, default=4096)
 ap.add_argument("--instance", type=int, default=0)
 ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--gate", action="store_true", help="MoE-side gating (forward_gated)")
 a = ap.parse_args()
 T = a.tokens_per_gpu * a.moe
 dev = torch.device("cuda", 0)
@@ -28,13 +29,17 @@ layer.set_weights(*build_weight_store(layer, seed=1))
 ex = torch.from_numpy(J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, 8, 0x30, T * 1000).experts).to(dev)
 x, gw = make_inputs(T, 8, 2048, 3, dev)
 out = torch.empty_like(x)
+if a.gate:
+    from paper_2512_13525_b200.moe import router_weights
+    layer.set_router(router_weights(128, 2048, 13, dev))
+fwd = (lambda: layer.forward_gated(x, out=out)) if a.gate else (lambda: layer.forward(x, ex, gw, out=out))
 for _ in range(a.steps):
-    layer.forward(x, ex, gw, out=out)
+    fwd()
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
 for _ in range(a.steps):
-    layer.forward(x, ex, gw, out=out)
+    fwd()
 e.record()
 torch.cuda.synchronize()
 print(f"T={T} instance {a.instance}/{a.moe}: {s.elapsed_time(e) / a.steps * 1e3:.1f} us/step (graph)")
