@@ -16,17 +16,21 @@
 // rows x N columns.  Per SM and k-block that is 32 KB written by TMA and 32 KB
 // read by the MMAs — half the smem traffic of two independent M=128 tiles,
 // which capped the single-CTA version at ~58% of the tensor pipe (profiles/).
-//   SWIGLU  CTA r's 128 rows = 64 gate rows + the 64 up rows of the same
-//           features (two TMA boxes), so the epilogue pairs lanes l and l+64
-//           through a small smem exchange and writes h for 64 features.
+//   SWIGLU  CTA r's 128 rows = 8 blocks of (8 gate rows, the 8 up rows of the
+//           same features), loaded by one 4-D TMA box, so a 16x256b TMEM load
+//           hands each epilogue thread gate and up of one feature and h is
+//           formed in registers for 64 features per CTA.
 //   PLAIN   CTA r's 128 rows = 128 consecutive rows of the down projection.
-// Per CTA: warp 0 TMA producer, warp 1 TMEM owner (+ the MMA issuer in the
-// leader CTA), warps 2-5 epilogue (tcgen05.ld -> math -> bf16 -> smem ->
-// coalesced 16-B stores).  6-stage smem ring, 2 TMEM accumulators of 256
-// columns.  Persistent: 74 pairs draw tiles from a global counter (dynamic
-// scheduling: a pair that drew a cheap tile draws the next one sooner) over the
-// tile list that the scheduler kernel wrote to device memory (group_off,
-// tile_off) — no host sync.
+// Per CTA (352 threads): warp 0 weight (A) producer + tile fetch, warp 1 TMEM
+// owner (+ the MMA issuer in the leader CTA), warps 2-9 epilogue (tcgen05.ld ->
+// math -> bf16 -> stmatrix.trans -> TMA store), warp 10 token-row (B)
+// producer; producer/MMA roles run as whole warps and issue via elect.sync.
+// Smem ring of 6 stages (256-row tiles) or 9 (decode, 64-row tiles), TMEM
+// double-buffered accumulators of 256 columns.  Persistent: 74 pairs draw
+// tiles from a global counter (dynamic scheduling: a pair that drew a cheap
+// tile draws the next one sooner) over the tile list that the scheduler
+// kernel wrote to device memory (group_off, tile_off) — no host sync; the
+// leader publishes each index to both CTAs through a small smem queue.
 #include <cuda_bf16.h>
 
 #include <algorithm>
