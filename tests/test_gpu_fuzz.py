@@ -1,0 +1,67 @@
+"""Seeded fuzz of the whole layer (K1 -> K3 -> K4 -> K5) against the fp32
+oracle over random shapes, replica maps, instance filters, shared experts and
+step sizes — both GEMM regimes (64- and 256-row tiles), ragged groups, empty
+instances.  JANUS_FUZZ_CASES sets the case count (default 64, a few
+seconds; 3000 cases ran clean on a B200).  Tolerances as in test_gpu_moe.py."""
+import os
+
+import numpy as np
+import pytest
+
+from test_gpu_moe import check_close, make_layer, oracle_layer_out, run, u16  # noqa: F401
+from oracle import bf16_to_f32
+
+pytestmark = pytest.mark.gpu
+CASES = int(os.environ.get("JANUS_FUZZ_CASES", "64"))
+
+
+def random_map(J, rng, E, N):
+    """Every expert on 1..min(3, N) distinct instances, capacity = the most
+    loaded instance (a valid reference ReplicaMap)."""
+    hosts = []
+    for _ in range(E):
+        r = int(rng.integers(1, min(3, N) + 1))
+        hosts.append(sorted(rng.choice(N, r, replace=False).tolist()))
+    cap = max(1, max(sum(g in h for h in hosts) for g in range(N)))
+    return J.ReplicaMap.from_hosts(N, cap, hosts)
+
+
+@pytest.fixture(scope="module")
+def J():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2512_13525_b200 as J
+    return J
+
+
+@pytest.mark.parametrize("case", range(CASES))
+def test_layer_fuzz(J, oracle, case):
+    import torch
+    from paper_2512_13525_b200.moe import expert_weights
+    rng = np.random.default_rng(1000 + case)
+    E = int(rng.choice([8, 16, 40, 64, 128]))
+    k = int(rng.choice([k_ for k_ in (1, 2, 4, 6, 8) if k_ <= E]))
+    d_h = int(rng.choice([256, 512, 768]))
+    d_e = int(rng.choice([128, 256, 384]))
+    # step sizes on both sides of the 28-rows-per-expert tile crossover
+    T = int(rng.choice([1, 3, int(rng.integers(4, 120)), int(rng.integers(120, 900))]))
+    N = int(rng.choice([1, 2, 3]))
+    rm = random_map(J, rng, E, N)
+    instance = -1 if N == 1 or rng.random() < 0.5 else int(rng.integers(0, N))
+    shared = bool(rng.random() < 0.25) and instance <= 0
+    pat = (J.RoutingPattern.zipf(E, float(rng.choice([0.0, 1.0, 1.5]))) if rng.random() < 0.7
+           else J.RoutingPattern.gaussian(E, 0.2))
+    b = J.gen_batch(pat, T, k, int(rng.integers(1 << 30)), case)
+    layer = make_layer(J, rm, d_h, d_e, max(T, 1), k, seed=case + 1, instance=instance)
+    if shared:
+        wg, wu, wd = expert_weights(E + 1, d_h, d_e, case + 3, "cuda")
+        layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
+    x, ex, gw, out = run(J, layer, b.experts, T, seed=case + 7)
+    tokens = np.unique(np.concatenate([[0, T - 1], rng.integers(0, T, 24)]))
+    ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens)
+    if shared:
+        ref += oracle.expert_swiglu(u16(x)[tokens], u16(wg), u16(wu), u16(wd), round_h=True,
+                                    nthreads=8)
+    what = (f"case {case}: E={E} k={k} d_h={d_h} d_e={d_e} T={T} N={N} instance={instance} "
+            f"shared={shared}")
+    check_close(bf16_to_f32(u16(out))[tokens], ref, what)
