@@ -1,8 +1,9 @@
-"""Seeded fuzz of the whole layer (K1 -> K3 -> K4 -> K5) against the fp32
-oracle over random shapes, replica maps, instance filters, shared experts and
-step sizes — both GEMM regimes (64- and 256-row tiles), ragged groups, empty
-instances.  JANUS_FUZZ_CASES sets the case count (default 64, a few
-seconds; 3000 cases ran clean on a B200).  Tolerances as in test_gpu_moe.py."""
+"""Seeded fuzz against the oracle.  The whole layer (K1 -> K3 -> K4 -> K5) vs
+the fp32 oracle over random shapes, replica maps, instance filters, shared
+experts and step sizes — both GEMM regimes (64- and 256-row tiles), ragged
+groups, empty instances (tolerances as in test_gpu_moe.py); the scheduler
+bit-exact over random maps and step sizes.  JANUS_FUZZ_CASES sets the case
+count per test (default 64, a few seconds; 3000 cases ran clean on a B200)."""
 import os
 
 import numpy as np
@@ -65,3 +66,36 @@ def test_layer_fuzz(J, oracle, case):
     what = (f"case {case}: E={E} k={k} d_h={d_h} d_e={d_e} T={T} N={N} instance={instance} "
             f"shared={shared}")
     check_close(bf16_to_f32(u16(out))[tokens], ref, what)
+
+
+@pytest.mark.parametrize("case", range(CASES))
+def test_scheduler_fuzz(J, oracle, case):
+    """K1+K2 bit-exact vs the oracle over random maps (1-40 instances, so the
+    warp greedy and the N > 32 path), expert counts and step sizes spanning
+    every cluster size (1-16 CTAs), AEBS and the random policy."""
+    from oracle import POLICY_RANDOM, CSRMap
+    rng = np.random.default_rng(5000 + case)
+    E = int(rng.choice([8, 16, 64, 128, 200, 256]))
+    N = int(rng.choice([1, 2, 3, 6, 8, 16, 33, 40]))
+    k = int(rng.choice([k_ for k_ in (1, 2, 4, 8) if k_ <= E]))
+    T = int(rng.choice([0, 1, int(rng.integers(2, 300)), int(rng.integers(300, 6000))]))
+    rm = random_map(J, rng, E, N)
+    pat = J.RoutingPattern.zipf(E, float(rng.choice([0.0, 1.0, 1.2])))
+    b = J.gen_batch(pat, T, k, int(rng.integers(1 << 30)), case)
+    m = CSRMap(rm.num_experts, rm.num_instances, rm.slots_per_instance, *rm.csr())
+    sched = J.Scheduler(rm)
+    try:
+        what = f"case {case}: E={E} N={N} k={k} T={T}"
+        a = sched.schedule(b)
+        ref = oracle.schedule(b.experts, T, k, m)
+        for f in ("instance", "replica", "expert_instance", "load", "routed_tokens"):
+            assert np.array_equal(np.asarray(getattr(a, f)), np.asarray(getattr(ref, f))), \
+                f"{what}: {f}"
+        seed = int(rng.integers(1 << 30))
+        a = sched.schedule_random(b, seed)
+        ref = oracle.schedule(b.experts, T, k, m, policy=POLICY_RANDOM, seed=seed)
+        for f in ("instance", "replica", "expert_instance", "load", "routed_tokens"):
+            assert np.array_equal(np.asarray(getattr(a, f)), np.asarray(getattr(ref, f))), \
+                f"{what} (random): {f}"
+    finally:
+        sched.close()
