@@ -2,7 +2,8 @@
 the fp32 oracle over random shapes, replica maps, instance filters, shared
 experts and step sizes — both GEMM regimes (64- and 256-row tiles), ragged
 groups, empty instances (tolerances as in test_gpu_moe.py); the scheduler
-bit-exact over random maps and step sizes.  JANUS_FUZZ_CASES sets the case
+bit-exact over random maps and step sizes; the gating kernel over random
+shapes.  JANUS_FUZZ_CASES sets the case
 count per test (default 64, a few seconds; 3000 cases ran clean on a B200)."""
 import os
 
@@ -99,3 +100,24 @@ def test_scheduler_fuzz(J, oracle, case):
                 f"{what} (random): {f}"
     finally:
         sched.close()
+
+
+@pytest.mark.parametrize("case", range(CASES))
+def test_gate_fuzz(J, oracle, case):
+    """The gating kernel over random (E, k, d_h, T): every split-K cluster
+    size and both epilogues, against the oracle's definition."""
+    import torch
+    from test_gpu_gate import _check
+    from paper_2512_13525_b200.moe import MoELayer, make_inputs, router_weights
+    rng = np.random.default_rng(9000 + case)
+    E = int(rng.choice([16, 32, 48, 64, 128, 160, 256]))
+    k = int(rng.choice([k_ for k_ in (1, 2, 4, 8, 16) if k_ <= E]))
+    d_h = int(rng.choice([256, 512, 1024, 2048]))
+    T = int(rng.choice([1, int(rng.integers(2, 200)), int(rng.integers(200, 3000))]))
+    rm = J.ReplicaMap.from_hosts(1, E, [[0]] * E)
+    layer = MoELayer(rm, 256, 128, max(T, 1), k, device=0)
+    x, _ = make_inputs(T, k, d_h, case + 5, "cuda")
+    wr = router_weights(E, d_h, case + 9, "cuda")
+    ex, gw = layer.gate(x, wr)
+    torch.cuda.synchronize()
+    _check(oracle, x, wr, k, ex, gw)
