@@ -3,8 +3,9 @@ the fp32 oracle over random shapes, replica maps, instance filters, shared
 experts and step sizes — both GEMM regimes (64- and 256-row tiles), ragged
 groups, empty instances (tolerances as in test_gpu_moe.py); the scheduler
 bit-exact over random maps and step sizes; the gating kernel over random
-shapes.  JANUS_FUZZ_CASES sets the case
-count per test (default 64, a few seconds; 3000 cases ran clean on a B200)."""
+shapes; the activation statistics bit-exact vs the reference.
+JANUS_FUZZ_CASES sets the case count per test (default 64, seconds; on a
+B200 3000 layer, 1000 scheduler, 400 gate and 300 stats cases ran clean)."""
 import os
 
 import numpy as np
@@ -121,3 +122,26 @@ def test_gate_fuzz(J, oracle, case):
     ex, gw = layer.gate(x, wr)
     torch.cuda.synchronize()
     _check(oracle, x, wr, k, ex, gw)
+
+
+@pytest.mark.parametrize("case", range(CASES))
+def test_stats_fuzz(J, ref, case):
+    """Device ActivationStats bit-exact vs the compiled reference over random
+    expert counts, windows and step sequences (empty steps included)."""
+    import torch
+    from test_gpu_stats import _steps
+    from paper_2512_13525_b200.moe import ActivationStats
+    rng = np.random.default_rng(12000 + case)
+    E = int(rng.choice([1, 2, 7, 32, 33, 100, 128, 256]))
+    k = int(rng.choice([k_ for k_ in (1, 2, 4, 8) if k_ <= E]))
+    W = int(rng.integers(1, 10))
+    steps = _steps(E, k, int(rng.integers(1, 3 * W + 6)), case)
+    st = ActivationStats(E, W)
+    dev = torch.device("cuda", 0)
+    for ex in steps:
+        st.record_batch(torch.from_numpy(np.ascontiguousarray(ex, np.int32)).to(dev), k)
+    counts, coact, rec = st.read()
+    rc, rco = ref.stats(E, W, [np.unique(ex) for ex in steps])
+    np.testing.assert_array_equal(counts, rc)
+    np.testing.assert_array_equal(coact.reshape(-1), rco)
+    assert rec == min(len(steps), W)
