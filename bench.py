@@ -90,7 +90,7 @@ def peaks():
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("clocks.sm,clocks.max.sm,power.draw.instant,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -128,8 +128,16 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[2]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "power_w": float(np.median(pw)) if pw else None,  # instantaneous draw
+                "power_max_w": max(pw) if pw else None,
                 "samples": len(self.rows)}
 
 
