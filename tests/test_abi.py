@@ -133,3 +133,16 @@ def test_config_maps_load(J):
         m = J.config_map(name)
         m.validate()
         assert m.num_experts in (64, 128, 256)
+
+
+def test_build_entry_does_not_need_the_library():
+    """__graft_entry__.build() must work on a fresh checkout: it loads build.py by
+    path without importing the package (whose import loads libjanus_b200.so)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import __graft_entry__ as g; "
+            "m = g._build_module(); assert callable(m.build); "
+            "assert 'paper_2512_13525_b200' not in sys.modules" % ROOT)
+    env = dict(os.environ, JANUS_LIB="/nonexistent/libjanus_b200.so")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
