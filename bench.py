@@ -570,12 +570,30 @@ def run_box(args):
     dist.barrier()
     # the scheduler every MoE GPU runs (replicated, on all T*k slots of the step)
     sched_us = layer.sched.time_schedule(batches[0], T, K_TOP, reps=51) if layer is not None else 0.0
-    tvec = torch.tensor([ms, ffn[1], float(launches), disp_ms, moe_ms, comb_ms, sched_us],
+    # algorithmic bytes of this MoE GPU's grouped GEMMs per step:
+    # its activated replicas' weights + its routed rows in and out, averaged over
+    # the batches the timed steps cycled through
+    alg_b = alg_f = 0.0
+    if layer is not None:
+        inst = plan.instance(rank)
+        per, perf = [], []
+        for b in gen_batches(T):
+            a = layer.sched.schedule(J.ActivationBatch(T, K_TOP, b))
+            A_loc, rows = int(a.load[inst]), int(a.routed_tokens[inst])
+            if SHARED:  # shared expert on this instance's even share of the tokens
+                A_loc, rows = A_loc + 1, rows + J.shard_tokens(T, M, inst)[1]
+            per.append(A_loc * 3 * D_H * D_E * 2 + rows * (D_H + D_E) * 2 * 2)
+            perf.append(6.0 * D_H * D_E * rows)
+        alg_b = float(np.mean([per[i % N_BATCHES] for i in range(args.steps)]))
+        alg_f = float(np.mean([perf[i % N_BATCHES] for i in range(args.steps)]))
+    tvec = torch.tensor([ms, ffn[1], float(launches), disp_ms, moe_ms, comb_ms, sched_us, alg_b, alg_f],
                         device=dev)
     allv = [torch.zeros_like(tvec) for _ in range(ws)]
     dist.all_gather(allv, tvec)
     ms_max = max(float(v[0]) for v in allv)
     ffn_ms = max(float(v[1]) for v in allv)  # slowest MoE GPU's grouped GEMMs
+    slow = max(range(ws), key=lambda r: float(allv[r][1]))
+    alg_slow, algf_slow = float(allv[slow][7]), float(allv[slow][8])
     launches_all = int(sum(float(v[2]) for v in allv))
     disp_ms = max(float(v[3]) for v in allv)
     moe_ms = max(float(v[4]) for v in allv)
@@ -655,6 +673,14 @@ def run_box(args):
         sends = plan.bytes_per_step(T, D_H, 0 if args.gate else K_TOP)
         send_bytes = sends[0][0]
         hbm, tf_burst, tf_sus, src = peaks()
+        gbs_slow = alg_slow / (ffn_ms / 1e3) / 1e9 if ffn_ms > 0 else 0.0
+        tfs_slow = algf_slow / (ffn_ms / 1e3) / 1e12 if ffn_ms > 0 else 0.0
+        tf_peak = tf_sus or tf_burst
+        hbm_bound = gbs_slow / hbm >= tfs_slow / tf_peak
+        roof = ({"bound": "hbm", "achieved": gbs_slow, "peak": hbm, "unit": "GB/s",
+                 "frac": gbs_slow / hbm} if hbm_bound else
+                {"bound": "tensor", "achieved": tfs_slow, "peak": tf_peak, "unit": "TFLOP/s",
+                 "frac": tfs_slow / tf_peak})
         line = {
             "metric": "moe_layer_tokens_per_s_per_gpu", "value": value, "unit": "tokens/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -682,9 +708,14 @@ def run_box(args):
                                  "the rows",
                        "l2": "inputs > L2 (weights streamed)"},
             "tokens_per_s_per_gpu": value / ws, "tokens_per_s_per_moe_gpu": value / M,
-            "roofline": {"bound": "hbm", "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
-                         "ffn_us_per_step": ffn_ms * 1e3, "achieved": None, "peak": hbm,
-                         "unit": "GB/s", "frac": None, "traffic": None,
+            "roofline": {**roof, "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
+                         "ffn_us_per_step": ffn_ms * 1e3,
+                         "traffic": None, "alg_bytes_per_step": alg_slow,
+                         "alg_flops_per_step": algf_slow, "hbm_frac": gbs_slow / hbm,
+                         "tensor_frac": tfs_slow / tf_peak,
+                         "how": "library CUDA events around both grouped-GEMM launches of "
+                                "every step on the MoE GPU with the largest FFN time; bytes "
+                                "from that GPU's own schedule of the same batches",
                          "peak_source": f"{src} (MEASURED_PEAKS.json)"},
             "nvlink": {"transport": box.transport,
                        # P2P: the attention GPU stores each row once per MoE GPU;
