@@ -313,3 +313,26 @@ def test_replica_map_reconfiguration(J, oracle):
     b = J.gen_batch(J.RoutingPattern.zipf(48, 1.0), 200, 4, 2, 0)
     x, ex, gw, out = run(J, layer, b.experts, 200)
     check_close(bf16_to_f32(u16(out)), oracle_layer_out(oracle, layer, x, ex, gw), "after")
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 6, 8])
+def test_box_map_full_step(J, oracle, M):
+    """The MoE side of `bench.py --gpus N` on one GPU: the c2_m{M} map (the
+    reference placement for M MoE instances, BoxPlan.for_gpus: M = 1, 3, 6 at
+    N = 2, 4, 8) at the box's full step, T = 4096·M tokens of the c2 shape.
+    The scheduler is bit-exact vs the oracle on all T·8 slots; the last
+    instance's partial layer output is within tolerance on a token sample."""
+    rm = J.config_map(f"c2_m{M}")
+    T, k = 4096 * M, 8
+    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, k, 0x30, T * 1000)
+    layer = make_layer(J, rm, 2048, 768, T, k, instance=M - 1)
+    off, hosts, rid = layer.sched._csr
+    m = CSRMap(rm.num_experts, rm.num_instances, rm.slots_per_instance, off, hosts, rid)
+    a = layer.sched.schedule(J.ActivationBatch(T, k, b.experts))
+    ref = oracle.schedule(b.experts, T, k, m)
+    for f in ("instance", "replica", "expert_instance", "load", "routed_tokens"):
+        assert np.array_equal(getattr(a, f), getattr(ref, f)), f"M={M}: {f}"
+    x, ex, gw, out = run(J, layer, b.experts, T)
+    tokens = np.arange(0, T, T // 48)
+    refo = oracle_layer_out(oracle, layer, x, ex, gw, tokens=tokens)
+    check_close(bf16_to_f32(u16(out))[tokens], refo, f"c2_m{M} instance {M - 1}")
