@@ -150,3 +150,27 @@ def test_box_protocol_gloo(world, n_attn):
     assert all(ok for _, _, ok, _ in res)
     moe = [inst for role, _, _, inst in res if role == "moe"]
     assert all(m_ == moe[0] for m_ in moe)  # sync-free: identical assignments everywhere
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])  # the N of the driver's scaling run
+def test_bench_box_plans(n):
+    """The splits `bench.py --gpus n` launches (BoxPlan.for_gpus: 1 attention GPU
+    per 4, the paper's 2A+6E box at 8) and the MoE-only box: roles cover every
+    rank once, attention shards tile the step exactly (comm.cpp:76-81), and the
+    replica map each split needs ships in the package."""
+    import paper_2512_13525_b200 as J
+    from paper_2512_13525_b200.dist import BoxPlan
+    p = BoxPlan.for_gpus(n)
+    assert p.n_attn == max(1, n // 4) and p.n_attn + p.n_moe == n == p.world
+    assert [p.instance(r) for r in range(n) if p.is_moe(r)] == list(range(p.n_moe))
+    assert sum(p.is_attention(r) for r in range(n)) == p.n_attn
+    for Tn in (4096 * p.n_moe, 4096 * p.n_moe + 3, 1):
+        spans = [p.shard(Tn, a) for a in range(p.n_attn)]
+        assert spans[0][0] == 0 and sum(c for _, c in spans) == Tn
+        assert all(f0 + c0 == f1 for (f0, c0), (f1, _) in zip(spans, spans[1:]))
+        assert p.owner(Tn, Tn - 1) == max(a for a, (_, c) in enumerate(spans) if c)
+    for M in (p.n_moe, n):  # split box and MoE-only box (BoxPlan.moe_only(n))
+        m = J.config_map(f"c2_m{M}") if M > 1 else J.config_map("c2")
+        assert m.num_instances == M and m.num_experts == 128
+    q = BoxPlan.moe_only(n)
+    assert all(q.is_attention(r) and q.is_moe(r) and q.instance(r) == r for r in range(n))
