@@ -38,7 +38,9 @@ typedef enum {
   JANUS_EUNKNOWN_EXPERT = 2, /* aebs.cpp:22-25 "unknown-expert: ..." */
   JANUS_ECUDA = 3,           /* CUDA runtime/driver failure */
   JANUS_ESTATE = 4,          /* call order: no map / no weights / not reserved */
-  JANUS_EUNSUPPORTED = 5     /* shape outside this build's kernel limits */
+  JANUS_EUNSUPPORTED = 5,    /* shape outside this build's kernel limits */
+  JANUS_EPEER = 6            /* box exchange: a peer rank never published its
+                                step (bounded wait expired) or failed it */
 } janus_status;
 
 typedef enum {
@@ -233,6 +235,13 @@ janus_status janus_xfer_connect(janus_ctx *ctx, const uint8_t *handles /* world 
 janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                                        const float *d_gate_w, int64_t num_tokens, uint64_t epoch,
                                        void *stream);
+/* device, attention rank, routed transport only (optional): the routing phase
+ * of janus_attn_dispatch_async alone — this shard's ids and gate weights into
+ * every rank, flag.  A later dispatch of the same epoch then skips it; callers
+ * that drive several ranks from one stream call it on every attention rank
+ * first (each dispatch waits for every shard's routing). */
+janus_status janus_attn_route_async(janus_ctx *ctx, const int32_t *d_experts, const float *d_gate_w,
+                                    int64_t num_tokens, uint64_t epoch, void *stream);
 /* device, MoE rank: wait for every shard of `epoch`, run K1-K4 on the received
  * step, and push this instance's per-token partial sums to their owners. */
 janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t num_tokens, uint64_t epoch,
@@ -243,6 +252,32 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t num_t
                                       uint64_t epoch, void *stream);
 /* host: 1 if a wait exceeded its bound (a peer never published). */
 janus_status janus_xfer_status(janus_ctx *ctx, int *timed_out);
+/* host (synchronises the device): the first failed step this rank saw since
+ * the last check — its own, or on the attention side any MoE rank's (each MoE
+ * rank publishes its scheduler status with its combine flag).  JANUS_OK,
+ * JANUS_EUNKNOWN_EXPERT with the reference message in janus_last_error
+ * (aebs.cpp:22-25), or JANUS_EPEER (a bounded wait expired).  A failed step's
+ * later kernels skip their work; the owners' output rows of it are zeros. */
+janus_status janus_xfer_check(janus_ctx *ctx);
+/* Instrumentation: device address of this rank's received token rows
+ * [max_tokens][d_h] bf16 in epoch's slot (MoE ranks: the dispatch target). */
+janus_status janus_xfer_recv_rows(const janus_ctx *ctx, uint64_t epoch, void **rows);
+/* Bound of every flag wait of this endpoint (default 20 s). */
+janus_status janus_xfer_set_timeout(janus_ctx *ctx, uint64_t timeout_ns);
+/* Same-process connect (all ranks' contexts in one process, on one or several
+ * devices): peers[r] = rank r's context, configured for the same box; replaces
+ * the IPC handle exchange.  Kernels that wait on one another must then still
+ * be enqueued in causal order (a rank's wait only after its producers). */
+janus_status janus_xfer_connect_local(janus_ctx *ctx, janus_ctx *const *peers);
+/* Routed transport (0: broadcast, the default; 1: routed), after configure, on
+ * every rank.  Routed: each attention rank ships its shard's routing to every
+ * rank, runs the scheduler over the whole step (identical to the MoE ranks'),
+ * and sends each row only to the MoE ranks its slots were scheduled on
+ * (north_star's per-GPU buffers; StepTraffic, comm.hpp:20-39); each MoE rank
+ * pushes partial sums only for the tokens it computed.  Needs the replica map
+ * on the attention ranks' contexts too (janus_set_replica_map), routing shipped
+ * (no MoE-side gating) and no shared expert; point to point only (no NVLS). */
+janus_status janus_xfer_set_transport(janus_ctx *ctx, int routed);
 /* NVLS multicast transport (optional, after janus_xfer_connect on every rank):
  * rows, routing and partial sums then move through one NVSwitch multicast
  * object — dispatch leaves an attention GPU once instead of once per MoE GPU,

@@ -12,10 +12,10 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("JANUS_LIB") or os.path.join(PKG, "libjanus_b200.so")  # override: A/B runs
 
-OK, EINVAL, EUNKNOWN_EXPERT, ECUDA, ESTATE, EUNSUPPORTED = range(6)
+OK, EINVAL, EUNKNOWN_EXPERT, ECUDA, ESTATE, EUNSUPPORTED, EPEER = range(7)
 POLICY_AEBS, POLICY_RANDOM = 0, 1
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "EUNKNOWN_EXPERT", 3: "ECUDA", 4: "ESTATE",
-                5: "EUNSUPPORTED"}
+                5: "EUNSUPPORTED", 6: "EPEER"}
 
 # Every entry point include/janus_b200.h declares (checked by tests/test_abi.py).
 SYMBOLS = (
@@ -32,7 +32,9 @@ SYMBOLS = (
     "janus_stats_record_async", "janus_stats_read", "janus_stats_status",
     "janus_moe_layer_host_async", "janus_moe_host_sync", "janus_moe_set_shared",
     "janus_moe_set_shared_split",
-    "janus_xfer_configure_colocated",
+    "janus_xfer_configure_colocated", "janus_xfer_check", "janus_xfer_set_timeout",
+    "janus_xfer_connect_local", "janus_xfer_set_transport", "janus_attn_route_async",
+    "janus_xfer_recv_rows",
 )
 
 
@@ -98,6 +100,12 @@ def _load() -> C.CDLL:
     L.janus_moe_set_shared.argtypes = [vp, vp, vp]
     L.janus_moe_set_shared_split.argtypes = [vp, i32]
     L.janus_xfer_configure_colocated.argtypes = [vp, i32, i32, i32, i32, i32]
+    L.janus_xfer_check.argtypes = [vp]
+    L.janus_xfer_set_timeout.argtypes = [vp, u64]
+    L.janus_xfer_connect_local.argtypes = [vp, vp]
+    L.janus_xfer_set_transport.argtypes = [vp, i32]
+    L.janus_attn_route_async.argtypes = [vp, vp, vp, i64, u64, vp]
+    L.janus_xfer_recv_rows.argtypes = [vp, u64, P(vp)]
     return L
 
 

@@ -192,6 +192,24 @@ struct Slots<0> {
   }
 };
 
+// A rejected step (unknown expert, or the exchange aborted it) still leaves a
+// layout the layer's later kernels can run on safely: no replica groups, no
+// GEMM tiles, every slot unrouted.  K3 / K5 also check status[0] and skip.
+// Called by every thread of one CTA.
+__device__ void write_error_layout(const SchedArgs &a, int status, int bad) {
+  const int R = a.map.R;
+  for (int q = threadIdx.x; q <= R; q += kSchedThreads) {
+    if (a.out.group_off) a.out.group_off[q] = 0;
+    if (a.tile_off) a.tile_off[q] = 0;
+  }
+  if (a.shared_off && threadIdx.x < 4) a.shared_off[threadIdx.x] = 0;
+  for (int s = threadIdx.x; s < a.S; s += kSchedThreads) a.out.instance[s] = -1;
+  if (threadIdx.x == 0) {
+    a.out.status[0] = status;
+    a.out.status[1] = bad;
+  }
+}
+
 template <int MAXIT>
 __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -205,6 +223,11 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   const bool leader = crank == 0;  // writes the per-expert / per-instance outputs
   uint64_t *trace = leader ? a.trace : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
+  // the box exchange aborted this step (a peer never published its rows)
+  if (a.abort_flag && *a.abort_flag) {
+    if (leader) write_error_layout(a, JANUS_EPEER, 0);
+    return;  // before any cluster barrier: every CTA reads the same flag
+  }
 
   // routed counts fit 32 bits (S < 2^31): 32-bit shared atomics are native.
   unsigned *routed = reinterpret_cast<unsigned *>(smem);        // [N]
@@ -310,10 +333,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   }
   cluster_arrive();  // our reads of remote smem are done (wait before exit)
   if (bad != INT_MAX) {
-    if (leader && tid == 0) {
-      a.out.status[0] = JANUS_EUNKNOWN_EXPERT;
-      a.out.status[1] = bad;
-    }
+    if (leader) write_error_layout(a, JANUS_EUNKNOWN_EXPERT, bad);
     cluster_wait();
     return;
   }
@@ -333,10 +353,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   }
   __syncthreads();
   if (s_bad != INT_MAX) {
-    if (leader && tid == 0) {
-      a.out.status[0] = JANUS_EUNKNOWN_EXPERT;
-      a.out.status[1] = s_bad;
-    }
+    if (leader) write_error_layout(a, JANUS_EUNKNOWN_EXPERT, s_bad);
     cluster_wait();
     return;
   }

@@ -63,6 +63,8 @@ void free_assign(janus_assignment &a) {
   a = janus_assignment{};
 }
 
+// Allocated zeroed: a layer call that fails before K1 writes them (or a
+// reconfigured context) never reads recycled bytes.
 cudaError_t alloc_assign(janus_assignment &a, int S, int E, int N, int R) {
   cudaError_t e;
   if ((e = dalloc(&a.instance, S)) || (e = dalloc(&a.replica, S)) ||
@@ -70,6 +72,16 @@ cudaError_t alloc_assign(janus_assignment &a, int S, int E, int N, int R) {
       (e = dalloc(&a.routed_tokens, N)) || (e = dalloc(&a.expert_tokens, E)) ||
       (e = dalloc(&a.slot_row, S)) || (e = dalloc(&a.row_slot, S)) ||
       (e = dalloc(&a.group_off, R + 1)) || (e = dalloc(&a.status, 2)))
+    return e;
+  const size_t s4 = sizeof(int32_t) * std::max(S, 1);
+  if ((e = cudaMemset(a.instance, 0, s4)) || (e = cudaMemset(a.replica, 0, s4)) ||
+      (e = cudaMemset(a.slot_row, 0, s4)) || (e = cudaMemset(a.row_slot, 0, s4)) ||
+      (e = cudaMemset(a.expert_instance, 0, sizeof(int32_t) * std::max(E, 1))) ||
+      (e = cudaMemset(a.load, 0, sizeof(int32_t) * std::max(N, 1))) ||
+      (e = cudaMemset(a.routed_tokens, 0, sizeof(int64_t) * std::max(N, 1))) ||
+      (e = cudaMemset(a.expert_tokens, 0, sizeof(int64_t) * std::max(E, 1))) ||
+      (e = cudaMemset(a.group_off, 0, sizeof(int32_t) * (R + 1))) ||
+      (e = cudaMemset(a.status, 0, sizeof(int32_t) * 2)))
     return e;
   return cudaSuccess;
 }
@@ -169,6 +181,8 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->xfer.local);
   dfree(ctx->xfer.counter);
   dfree(ctx->xfer.err);
+  free_assign(ctx->xfer.rws);
+  dfree(ctx->xfer.dmask);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -275,7 +289,7 @@ static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T
                                  int policy, uint64_t seed, const janus_assignment &out,
                                  int32_t *tile_off, cudaStream_t stream,
                                  int32_t *shared_off = nullptr, int shared_tile_n = 0,
-                                 int shared_rows = 0) {
+                                 int shared_rows = 0, const int *abort_flag = nullptr) {
   if (T < 0 || k <= 0 || (int64_t)T * k > (int64_t)1 << 30)
     return fail(ctx, JANUS_EINVAL, "batch: num_tokens must be >= 0 and top_k >= 1");
   if (policy != JANUS_POLICY_AEBS && policy != JANUS_POLICY_RANDOM)
@@ -301,6 +315,7 @@ static janus_status launch_sched(janus_ctx *ctx, const int32_t *d_experts, int T
   a.shared_off = shared_off;
   a.shared_tile_n = shared_tile_n;
   a.shared_rows = shared_rows;
+  a.abort_flag = abort_flag;
   cudaError_t e = janus::launch_schedule(a, stream);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "aebs_schedule_kernel");
   ctx->launches += 1;
@@ -456,6 +471,7 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   (void)m;
   CK(alloc_assign(ctx->ws, S, JANUS_MAX_EXPERTS, JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
   CK(dalloc(&ctx->ws_tile_off, JANUS_MAX_REPLICAS + 1));
+  CK(cudaMemset(ctx->ws_tile_off, 0, sizeof(int32_t) * (JANUS_MAX_REPLICAS + 1)));
   CK(cudaMalloc(&ctx->d_x, (size_t)max_tokens * d_h * 2));
   CK(cudaMalloc(&ctx->d_outbuf, (size_t)max_tokens * d_h * 2));
   CK(dalloc(&ctx->d_experts, S));
@@ -508,6 +524,7 @@ janus_status janus_moe_set_shared(janus_ctx *ctx, const void *w13, const void *w
     CK(dalloc(&ps.tile_ctr, 4));
     CK(cudaMemset(ps.tile_ctr, 0, 4 * sizeof(unsigned)));
     CK(dalloc(&ctx->shared_off, 4));
+    CK(cudaMemset(ctx->shared_off, 0, 4 * sizeof(int32_t)));
   }
   ps.q_begin = 0;
   ps.q_end = 1;
@@ -554,7 +571,7 @@ janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *w13
 static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                               const float *d_gate_w, int T, void *d_out,
                               const janus_assignment *assign, cudaStream_t s,
-                              unsigned long long push_epoch) {
+                              unsigned long long push_epoch, const int *abort_flag = nullptr) {
   janus_status st = check_ready(ctx);
   if (st != JANUS_OK) return st;
   if (!ctx->moe_ready) return fail(ctx, JANUS_ESTATE, "moe: weights not set");
@@ -611,12 +628,14 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
   janus::FfnPlan &ps = ctx->ffn_shared;
   if (shared) ps.tile_n = sh1 - sh0 <= 64 ? 64 : janus::kTileN;
   st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, ctx->ws_tile_off, s,
-                    shared ? ctx->shared_off : nullptr, shared ? ps.tile_n : 0, sh1 - sh0);
+                    shared ? ctx->shared_off : nullptr, shared ? ps.tile_n : 0, sh1 - sh0,
+                    abort_flag);
   if (st != JANUS_OK) return st;
   if (ev) CK(cudaEventRecord(ev[1], s));
   janus::FfnPlan &p = ctx->ffn;
   cudaError_t e = janus::launch_permute(d_x, a.slot_row, a.instance, ctx->instance, T * k, k,
-                                        p.d_h, p.xp, shared ? ps.xp : nullptr, sh0, sh1, s);
+                                        p.d_h, p.xp, shared ? ps.xp : nullptr, sh0, sh1, s,
+                                        a.status);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "permute_kernel");
   int launches = 0;
   if (ev) CK(cudaEventRecord(ev[2], s));
@@ -625,23 +644,31 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     e = janus::launch_ffn(ps, ctx->shared_off, ctx->shared_off + 2, s, &launches);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "grouped_gemm_kernel");
   if (ev) CK(cudaEventRecord(ev[3], s));
-  if (push_epoch && ctx->xfer.mc) {
-    // multicast: partial sums of this instance for every token into the own
-    // backing (the attention ranks' switch-reduced reads add them up), flag
+  if (push_epoch) {
+    // box exchange: this instance's per-token partial sums go to the tokens'
+    // owners — into this rank's multicast backing (NVLS: the owners'
+    // switch-reduced reads add them up) or pushed into the owners' regions
+    // (P2P / routed, K5 fused with the NVLink transfer) — then the step's
+    // status and the combine flag are published on every attention rank
     const janus::XferState &x = ctx->xfer;
-    e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
-                              reinterpret_cast<void *>(x.uc_va + x.mpart_off +
-                                                       janus::xfer_slot(push_epoch) * x.mslot),
-                              s, shared ? ps.y : nullptr, sh0, sh1);
-    if (e == cudaSuccess) e = janus::launch_signal_combine(x, push_epoch, s);
+    if (x.mc) {
+      e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
+                                reinterpret_cast<void *>(x.uc_va + x.mpart_off +
+                                                         janus::xfer_slot(push_epoch) * x.mslot),
+                                s, shared ? ps.y : nullptr, sh0, sh1, a.status);
+    } else {
+      if (shared && x.transport == janus::kXferRouted)
+        return fail(ctx, JANUS_EUNSUPPORTED,
+                    "moe: the shared expert needs a broadcast transport (P2P or NVLS)");
+      const janus::PushDst pd = janus::push_dst(x, push_epoch);
+      e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
+                                nullptr, s, shared ? ps.y : nullptr, sh0, sh1, a.status, &pd);
+    }
+    if (e == cudaSuccess) e = janus::launch_signal_combine(x, a.status, push_epoch, s);
     launches += 1;
-  } else if (push_epoch) {
-    if (shared) return fail(ctx, JANUS_EUNSUPPORTED, "moe: shared expert needs the NVLS transport");
-    e = janus::launch_combine_push(ctx->xfer, p.y, a.slot_row, a.instance, d_gate_w, T,
-                                   push_epoch, s);
   } else
     e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
-                              d_out, s, shared ? ps.y : nullptr, sh0, sh1);
+                              d_out, s, shared ? ps.y : nullptr, sh0, sh1, a.status);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
   ctx->launches += 2 + launches;  // permute, combine, GEMMs (launch_sched counts itself)
   return JANUS_OK;
@@ -701,6 +728,19 @@ janus_status janus_moe_layer_async(janus_ctx *ctx, const void *d_x, const int32_
 
 // ------------------------------------------------ box exchange (K6) -----
 
+static void xfer_release(janus_ctx *ctx) {
+  janus::XferState &x = ctx->xfer;
+  janus::mc_free(x, ctx->device);
+  if (x.local) cudaFree(x.local);
+  for (void *p : x.opened) cudaIpcCloseMemHandle(p);
+  dfree(x.counter);
+  dfree(x.err);
+  free_assign(x.rws);
+  dfree(x.dmask);
+  x = janus::XferState{};
+  ctx->xfer_ready = false;
+}
+
 static janus_status xfer_setup(janus_ctx *ctx, int n_attn, int n_moe, int rank, int max_tokens,
                                int d_h, int k, bool colocated) {
   if (!ctx) return JANUS_EINVAL;
@@ -711,13 +751,8 @@ static janus_status xfer_setup(janus_ctx *ctx, int n_attn, int n_moe, int rank, 
   if (world > 16 || n_moe > 32)
     return fail(ctx, JANUS_EUNSUPPORTED, "xfer: at most 16 ranks in one box");
   CK(cudaSetDevice(ctx->device));
+  xfer_release(ctx);
   janus::XferState &x = ctx->xfer;
-  janus::mc_free(x, ctx->device);
-  if (x.local) cudaFree(x.local);
-  for (void *p : x.opened) cudaIpcCloseMemHandle(p);
-  dfree(x.counter);
-  dfree(x.err);
-  x = janus::XferState{};
   x.rank = rank;
   x.world = world;
   x.moe0 = colocated ? 0 : n_attn;
@@ -729,13 +764,12 @@ static janus_status xfer_setup(janus_ctx *ctx, int n_attn, int n_moe, int rank, 
   x.L = janus::xfer_layout(n_attn, n_moe, max_tokens, d_h, k);
   CK(cudaMalloc(&x.local, x.L.bytes));
   CK(cudaMemset(x.local, 0, x.L.bytes));
-  CK(dalloc(&x.counter, 1));
-  CK(dalloc(&x.err, 1));
-  CK(cudaMemset(x.counter, 0, sizeof(unsigned)));
-  CK(cudaMemset(x.err, 0, sizeof(int)));
+  CK(dalloc(&x.counter, 2 * janus::kCounterKinds));
+  CK(dalloc(&x.err, janus::kErrWords));
+  CK(cudaMemset(x.counter, 0, sizeof(unsigned) * 2 * janus::kCounterKinds));
+  CK(cudaMemset(x.err, 0, sizeof(int) * janus::kErrWords));
   x.peer_base.assign(x.world, nullptr);
   x.peer_base[rank] = x.local;
-  ctx->xfer_ready = false;
   return JANUS_OK;
 }
 
@@ -747,6 +781,34 @@ janus_status janus_xfer_configure(janus_ctx *ctx, int n_attn, int n_moe, int ran
 janus_status janus_xfer_configure_colocated(janus_ctx *ctx, int n, int rank, int max_tokens,
                                             int d_h, int k) {
   return xfer_setup(ctx, n, n, rank, max_tokens, d_h, k, true);
+}
+
+janus_status janus_xfer_set_transport(janus_ctx *ctx, int routed) {
+  if (!ctx || !ctx->xfer.local) return fail(ctx, JANUS_ESTATE, "xfer: configure first");
+  if (routed != 0 && routed != 1) return fail(ctx, JANUS_EINVAL, "xfer: transport must be 0 or 1");
+  janus::XferState &x = ctx->xfer;
+  if (routed && x.mc)
+    return fail(ctx, JANUS_EINVAL, "xfer: the routed transport is point to point (no NVLS)");
+  if (routed && x.M > 32)
+    return fail(ctx, JANUS_EUNSUPPORTED, "xfer: routed transport needs <= 32 MoE ranks");
+  CK(cudaSetDevice(ctx->device));
+  if (routed && x.rank < x.A && !x.dmask) {
+    // attention side: the step's schedule (K1 over every shard's routing) and
+    // the destination masks of its tokens, per epoch slot
+    CK(alloc_assign(x.rws, (int)std::min<long long>(x.T_max * x.k, INT_MAX), JANUS_MAX_EXPERTS,
+                    JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
+    CK(dalloc(&x.dmask, 2 * x.L.ta_max));
+    CK(cudaMemset(x.dmask, 0, sizeof(uint32_t) * 2 * x.L.ta_max));
+  }
+  x.transport = routed ? janus::kXferRouted : janus::kXferP2P;
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_set_timeout(janus_ctx *ctx, uint64_t timeout_ns) {
+  if (!ctx || !ctx->xfer.local) return fail(ctx, JANUS_ESTATE, "xfer: configure first");
+  if (timeout_ns == 0) return fail(ctx, JANUS_EINVAL, "xfer: timeout must be > 0");
+  ctx->xfer.timeout_ns = timeout_ns;
+  return JANUS_OK;
 }
 
 janus_status janus_xfer_handle(const janus_ctx *ctx, uint8_t *handle) {
@@ -775,6 +837,46 @@ janus_status janus_xfer_connect(janus_ctx *ctx, const uint8_t *handles) {
   return JANUS_OK;
 }
 
+janus_status janus_xfer_connect_local(janus_ctx *ctx, janus_ctx *const *peers) {
+  if (!ctx || !ctx->xfer.local || !peers) return JANUS_ESTATE;
+  CK(cudaSetDevice(ctx->device));
+  janus::XferState &x = ctx->xfer;
+  for (int r = 0; r < x.world; ++r) {
+    const janus_ctx *p = peers[r];
+    if (!p || !p->xfer.local || p->xfer.world != x.world || p->xfer.rank != r ||
+        p->xfer.L.bytes != x.L.bytes)
+      return fail(ctx, JANUS_EINVAL, "xfer: peer " + std::to_string(r) +
+                                          " is not configured for this box");
+    if (p->device != ctx->device) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(p->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else if (e != cudaSuccess)
+        return cuda_fail(ctx, e, "cudaDeviceEnablePeerAccess");
+    }
+    x.peer_base[r] = p->xfer.local;
+  }
+  ctx->xfer_ready = true;
+  return JANUS_OK;
+}
+
+janus_status janus_attn_route_async(janus_ctx *ctx, const int32_t *d_experts, const float *d_gate_w,
+                                    int64_t T, uint64_t epoch, void *stream) {
+  if (!ctx || !ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: not connected");
+  janus::XferState &x = ctx->xfer;
+  if (x.rank >= x.A) return fail(ctx, JANUS_EINVAL, "xfer: routing from a non-attention rank");
+  if (x.transport != janus::kXferRouted)
+    return fail(ctx, JANUS_ESTATE, "xfer: routing phase of the routed transport only");
+  if (T < 0 || T > x.T_max || epoch == 0 || !d_experts || !d_gate_w)
+    return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens], epoch 0 or no routing");
+  cudaError_t e = janus::launch_route_push(x, d_experts, d_gate_w, T, epoch,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "route_push_kernel");
+  ctx->launches += 1;
+  x.routed_epoch = epoch;
+  return JANUS_OK;
+}
+
 janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                                        const float *d_gate_w, int64_t T, uint64_t epoch,
                                        void *stream) {
@@ -785,9 +887,43 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
     return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens] or epoch 0");
   if (!d_experts != !d_gate_w)
     return fail(ctx, JANUS_EINVAL, "xfer: pass both routing arrays, or neither (MoE-side gating)");
-  cudaError_t e = janus::launch_dispatch(x, d_x, d_experts, d_gate_w, T, epoch,
-                                         static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "dispatch_kernel");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (x.transport != janus::kXferRouted) {
+    cudaError_t e = janus::launch_dispatch(x, d_x, d_experts, d_gate_w, T, epoch, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "dispatch_kernel");
+    ctx->launches += 1;
+    return JANUS_OK;
+  }
+  // routed: the routing first (every rank), then K1 over the whole step here —
+  // identical to every MoE rank's — then each row only to its instances
+  if (!d_experts)
+    return fail(ctx, JANUS_EINVAL, "xfer: the routed transport needs the routing on the attention side");
+  if (!ctx->have_map)
+    return fail(ctx, JANUS_ESTATE, "xfer: the routed transport needs the replica map on attention ranks");
+  if (ctx->dmap.N != x.M)
+    return fail(ctx, JANUS_EINVAL, "xfer: replica map instances != MoE ranks");
+  cudaError_t e = cudaSuccess;
+  if (x.routed_epoch != epoch) {  // not pushed ahead by janus_attn_route_async
+    janus_status rs = janus_attn_route_async(ctx, d_experts, d_gate_w, T, epoch, stream);
+    if (rs != JANUS_OK) return rs;
+  }
+  const int32_t *full = d_experts;  // one attention rank: its shard is the step
+  const int *abort_flag = nullptr;
+  if (x.A > 1) {
+    e = janus::launch_wait(x, 2, epoch, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
+    ctx->launches += 1;
+    full = reinterpret_cast<const int32_t *>(static_cast<const unsigned char *>(x.local) +
+                                             x.L.ex_off + janus::xfer_slot(epoch) * x.L.slot_stride);
+    abort_flag = x.err + janus::kErrSkip + 2;
+  }
+  janus_assignment ra = x.rws;
+  ra.slot_row = ra.row_slot = ra.group_off = nullptr;
+  janus_status st = launch_sched(ctx, full, (int)T, x.k, JANUS_POLICY_AEBS, 0, ra, nullptr, s,
+                                 nullptr, 0, 0, abort_flag);
+  if (st != JANUS_OK) return st;
+  e = janus::launch_routed_dispatch(x, d_x, x.rws.instance, x.rws.status, T, epoch, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "routed_dispatch_kernel");
   ctx->launches += 1;
   return JANUS_OK;
 }
@@ -799,10 +935,13 @@ janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoc
     return fail(ctx, JANUS_EINVAL, "xfer: MoE rank must hold instance rank - n_attn");
   if (T < 0 || T > x.T_max || epoch == 0)
     return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens] or epoch 0");
+  if (ctx->router && x.transport == janus::kXferRouted)
+    return fail(ctx, JANUS_EINVAL, "xfer: MoE-side gating needs a broadcast transport");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = janus::launch_wait(x, true, epoch, s);
+  cudaError_t e = janus::launch_wait(x, 0, epoch, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
   ctx->launches += 1;
+  const int *abort_flag = x.err + janus::kErrSkip + 0;  // a shard never arrived
   if (ctx->router) {  // MoE-side gating: routing from the received rows
     unsigned char *base =
         x.mc ? reinterpret_cast<unsigned char *>(x.uc_va) + janus::xfer_slot(epoch) * x.mslot
@@ -811,19 +950,20 @@ janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoc
     janus_status gs = janus_gate_async(ctx, xr, ctx->router, T, ctx->d_h, ctx->dmap.E,
                                        ctx->top_k, ctx->d_experts, ctx->d_gw, stream);
     if (gs != JANUS_OK) return gs;
-    return layer_run(ctx, xr, ctx->d_experts, ctx->d_gw, (int)T, nullptr, nullptr, s, epoch);
+    return layer_run(ctx, xr, ctx->d_experts, ctx->d_gw, (int)T, nullptr, nullptr, s, epoch,
+                     abort_flag);
   }
   if (x.mc) {  // rows / routing landed in this rank's multicast backing
     unsigned char *base = reinterpret_cast<unsigned char *>(x.uc_va) + janus::xfer_slot(epoch) * x.mslot;
     return layer_run(ctx, base + x.mx_off, reinterpret_cast<const int32_t *>(base + x.mex_off),
                      reinterpret_cast<const float *>(base + x.mgw_off), (int)T, nullptr, nullptr,
-                     s, epoch);
+                     s, epoch, abort_flag);
   }
   unsigned char *base =
       static_cast<unsigned char *>(x.local) + janus::xfer_slot(epoch) * x.L.slot_stride;
   return layer_run(ctx, base + x.L.x_off, reinterpret_cast<const int32_t *>(base + x.L.ex_off),
                    reinterpret_cast<const float *>(base + x.L.gw_off), (int)T, nullptr, nullptr, s,
-                   epoch);
+                   epoch, abort_flag);
 }
 
 janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, uint64_t epoch,
@@ -831,16 +971,47 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, ui
   if (!ctx || !ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: not connected");
   const janus::XferState &x = ctx->xfer;
   if (x.rank >= x.A) return fail(ctx, JANUS_EINVAL, "xfer: combine on a non-attention rank");
+  if (T < 0 || T > x.T_max || epoch == 0)
+    return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens] or epoch 0");
   int64_t first = 0, Ta = 0;
   janus_shard_tokens(T, x.A, x.rank, &first, &Ta);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = janus::launch_wait(x, false, epoch, s);
+  cudaError_t e = janus::launch_wait(x, 1, epoch, s);
   if (e == cudaSuccess)
     e = x.mc ? janus::launch_reduce_mc(x, d_out, first, Ta, epoch, s)
              : janus::launch_reduce_partials(x, d_out, Ta, epoch, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, x.mc ? "reduce_mc_kernel" : "reduce_partials_kernel");
   ctx->launches += 2;
   return JANUS_OK;
+}
+
+janus_status janus_xfer_recv_rows(const janus_ctx *ctx, uint64_t epoch, void **rows) {
+  if (!ctx || !ctx->xfer.local || !rows) return JANUS_ESTATE;
+  const janus::XferState &x = ctx->xfer;
+  *rows = x.mc ? reinterpret_cast<void *>(x.uc_va + x.mx_off + janus::xfer_slot(epoch) * x.mslot)
+               : static_cast<unsigned char *>(x.local) + x.L.x_off +
+                     janus::xfer_slot(epoch) * x.L.slot_stride;
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_check(janus_ctx *ctx) {
+  if (!ctx || !ctx->xfer.err) return fail(ctx, JANUS_ESTATE, "xfer: configure first");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  int w[janus::kErrWords];
+  CK(cudaMemcpy(w, ctx->xfer.err, sizeof(w), cudaMemcpyDeviceToHost));
+  if (w[janus::kErrStatus] == JANUS_OK) return JANUS_OK;
+  const int st = w[janus::kErrStatus], bad = w[janus::kErrBad];
+  // report once: clear the sticky words (the timeout flag stays for janus_xfer_status)
+  CK(cudaMemset(ctx->xfer.err + janus::kErrStatus, 0, 2 * sizeof(int)));
+  if (st == JANUS_EUNKNOWN_EXPERT)
+    return fail(ctx, JANUS_EUNKNOWN_EXPERT,
+                "unknown-expert: batch references expert " + std::to_string(bad) +
+                    " with no replica in the map");
+  if (st == JANUS_EPEER)
+    return fail(ctx, JANUS_EPEER, "xfer: a peer rank never published its step (wait bound expired)");
+  return fail(ctx, (janus_status)st, "xfer: a step of the box failed (status " +
+                                         std::to_string(st) + ")");
 }
 
 janus_status janus_gate_async(janus_ctx *ctx, const void *d_x, const void *d_router, int64_t T,

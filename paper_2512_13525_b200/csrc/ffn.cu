@@ -36,9 +36,10 @@ constexpr int kWarpsPerBlock = 4;
 __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__restrict__ slot_row,
                                const int32_t *__restrict__ slot_inst, int instance, int T, int k,
                                int vec, uint4 *__restrict__ xp, uint4 *__restrict__ xp_shared,
-                               int sh0, int sh1) {
+                               int sh0, int sh1, const int32_t *__restrict__ status) {
   sm100::pdl_trigger();
   sm100::pdl_wait();  // slot_row / slot_inst from K1
+  if (status && status[0] != JANUS_OK) return;  // rejected step: no layout
   const int lane = threadIdx.x & 31;
   const int segs = (vec + 32 * kPermU - 1) / (32 * kPermU);
   const int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -95,12 +96,29 @@ __global__ void permute_kernel(const uint4 *__restrict__ x, const int32_t *__res
 // slot local — fewer registers, more warps; with the instance filter about k/M
 // of a token's slots are routed here and the ballot compaction keeps the loads
 // to the slots that exist).
+// Shard rule (comm.cpp:76-81): owner a of token t and the shard's first token.
+__device__ __forceinline__ void shard_of(long long T, int A, long long t, int &a, long long &first) {
+  const long long base = T / A, rem = T % A;
+  const long long big = rem * (base + 1);
+  if (t < big) {
+    a = (int)(t / (base + 1));
+    first = (long long)a * (base + 1);
+  } else {
+    a = (int)(rem + (t - big) / base);
+    first = big + (long long)(a - rem) * base;
+  }
+}
+
+// Push mode (push.A > 0, the box exchange): the partial sum of token t goes
+// straight into its owning attention rank's region over NVLink (the combine
+// fused with the transfer); skip_empty drops tokens with no slot here.
 template <int G>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
     combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
                    const int32_t *__restrict__ slot_inst, int instance,
                    const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out,
-                   const uint4 *__restrict__ y_shared, int sh0, int sh1) {
+                   const uint4 *__restrict__ y_shared, int sh0, int sh1,
+                   const int32_t *__restrict__ status, const PushDst push) {
   sm100::pdl_trigger();
   sm100::pdl_wait();  // y from the down GEMM
   const int lane = threadIdx.x & 31;
@@ -108,6 +126,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
   const int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (task >= T * segs) return;
   const int t = task / segs, c0 = (task % segs) * 32 * kCombU + lane;
+  uint4 *orow = out + (size_t)t * vec;
+  if (push.A > 0) {
+    int a;
+    long long first;
+    shard_of(T, push.A, t, a, first);
+    orow = reinterpret_cast<uint4 *>(push.base[a] + push.part_off) +
+           ((long long)push.g * push.ta_max + (t - first)) * vec;
+  }
+  if (status && status[0] != JANUS_OK) {  // rejected step: no y reads
+    if (push.A > 0) return;  // the error slot tells the owner (signal_combine_kernel)
+#pragma unroll
+    for (int u = 0; u < kCombU; ++u)   // defined zeros
+      if (c0 + 32 * u < vec) orow[c0 + 32 * u] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  bool any = y_shared && t >= sh0 && t < sh1;
   float acc[kCombU][8];
 #pragma unroll
   for (int u = 0; u < kCombU; ++u)
@@ -127,6 +161,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
     const int n = min(32, k - j0);
     // lanes holding a slot routed here, taken in ascending j, G per round
     unsigned m = __ballot_sync(0xffffffffu, lane < n && row >= 0);
+    any = any || m != 0;
     while (m) {
       uint4 v[G][kCombU];
       float wv[G];
@@ -184,6 +219,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
       }
     }
   }
+  if (push.skip_empty && !any) return;  // routed: nothing of t was computed here
 #pragma unroll
   for (int u = 0; u < kCombU; ++u) {
     const int c = c0 + 32 * u;
@@ -192,7 +228,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
     __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
 #pragma unroll
     for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(acc[u][2 * e], acc[u][2 * e + 1]);
-    out[(size_t)t * vec + c] = o;
+    orow[c] = o;
   }
 }
 
@@ -200,7 +236,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
 
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, int S, int k, int d_h, void *xp, void *xp_shared,
-                           int sh0, int sh1, cudaStream_t s) {
+                           int sh0, int sh1, cudaStream_t s, const int32_t *status) {
   if (S == 0) return cudaSuccess;
   const int T = S / k, vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kPermU - 1) / (32 * kPermU));
@@ -208,20 +244,23 @@ cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t
   return sm100::launch_pdl(permute_kernel, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
                            reinterpret_cast<const uint4 *>(x), slot_row, slot_instance, instance,
                            T, k, vec, reinterpret_cast<uint4 *>(xp),
-                           reinterpret_cast<uint4 *>(xp_shared), sh0, sh1);
+                           reinterpret_cast<uint4 *>(xp_shared), sh0, sh1, status);
 }
 
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
-                           cudaStream_t s, const void *y_shared, int sh0, int sh1) {
+                           cudaStream_t s, const void *y_shared, int sh0, int sh1,
+                           const int32_t *status, const PushDst *push) {
   if (T == 0) return cudaSuccess;
   const int vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kCombU - 1) / (32 * kCombU));
   const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  PushDst pd{};
+  if (push) pd = *push;
   return sm100::launch_pdl(combine_kernel<4>, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,
                            reinterpret_cast<const uint4 *>(y), slot_row, slot_instance, instance,
                            gate_w, T, k, vec, reinterpret_cast<uint4 *>(out),
-                           reinterpret_cast<const uint4 *>(y_shared), sh0, sh1);
+                           reinterpret_cast<const uint4 *>(y_shared), sh0, sh1, status, pd);
 }
 
 }  // namespace janus

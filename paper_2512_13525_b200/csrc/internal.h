@@ -36,6 +36,7 @@ struct SchedArgs {
   int32_t *shared_off;  // optional [4]: the shared expert's {0, rows} and {0, n-tiles}
   int shared_tile_n;
   int shared_rows;      // tokens this instance runs the shared expert on
+  const int *abort_flag;  // optional: non-zero -> reject the step (JANUS_EPEER)
 };
 
 inline int id_bits_for(int E) {
@@ -70,16 +71,28 @@ cudaError_t build_ffn_tensor_maps(FfnPlan &p);
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, int S, int k, int d_h, void *xp, void *xp_shared,
                            int sh0, int sh1,
-                           cudaStream_t s);
+                           cudaStream_t s, const int32_t *status = nullptr);
 // gate/up GEMM with fused SwiGLU, then the down GEMM; 2 launches.
 cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
                        cudaStream_t s, int *launches);
+// K5 push mode (box exchange): token t's partial sum goes to its owning
+// attention rank a (shard rule, comm.cpp:76-81) at part[g][t - first_a] of that
+// rank's region; skip_empty: tokens with no slot on this instance send nothing.
+constexpr int kPushMaxPeers = 16;
+struct PushDst {
+  unsigned char *base[kPushMaxPeers];  // attention ranks' regions (A == 0: local out)
+  size_t part_off;
+  long long ta_max;
+  int A, g, skip_empty;
+};
+
 // y_shared (optional): + y_shared[t - sh0] (weight 1) after the k routed
 // slots, for t in [sh0, sh1)
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
                            cudaStream_t s, const void *y_shared = nullptr, int sh0 = 0,
-                           int sh1 = 0);
+                           int sh1 = 0, const int32_t *status = nullptr,
+                           const PushDst *push = nullptr);
 
 // MoE-side gating (gate.cu): router GEMM + top-k + softmax of the top-k logits.
 bool gate_shape_ok(int d_h, int E, int k);
@@ -103,12 +116,29 @@ cudaError_t launch_stats_record(const StatsState &st, const int32_t *experts, lo
 // ranks [A, A+M) are MoE instances g = rank - A.  One exchange region per
 // rank, identical layout everywhere.
 struct XferLayout {
-  // x/ex/gw/part offsets are slot 0's; slot 1 (odd epochs) is + slot_stride, so
-  // two steps can be in flight (dispatch of step s+1 while step s computes)
-  size_t flag_dispatch_off, flag_combine_off, x_off, ex_off, gw_off, part_off, slot_stride, bytes;
+  // flags (u64, epoch-valued): dispatch[A] (rows landed), combine[M] (partial
+  // sums landed), route[A] (routing landed; routed transport).
+  size_t flag_dispatch_off, flag_combine_off, flag_route_off;
+  // x/ex/gw/part/err offsets are slot 0's; slot 1 (odd epochs) is + slot_stride,
+  // so two steps can be in flight (dispatch of step s+1 while step s computes).
+  // err[M] = {status, bad expert} of MoE instance g's step, written before its
+  // combine flag (a failed MoE step is reported on the attention ranks).
+  size_t x_off, ex_off, gw_off, part_off, err_off, slot_stride, bytes;
   long long ta_max;  // largest attention shard
 };
 XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k);
+
+enum XferTransport { kXferP2P = 0, kXferRouted = 1 };  // NVLS: XferState::mc
+
+// Device error words of one rank's exchange endpoint (x.err, int[8]).
+enum XferErr {
+  kErrTimeout = 0,  // sticky: a bounded wait expired
+  kErrStatus = 1,   // sticky: first failed step's status (a remote MoE step's, or this rank's)
+  kErrBad = 2,      // sticky: its bad expert id
+  kErrSkip = 3,     // + wait kind (0 dispatch, 1 combine, 2 route): this step's verdict of
+                    // that wait, 1 -> the step's later kernels skip their work
+  kErrWords = 8
+};
 
 struct XferState {
   int rank = -1, world = 0, A = 0, M = 0, d_h = 0, k = 0;
@@ -116,12 +146,20 @@ struct XferState {
   // shard owner and an MoE instance (janus_xfer_configure_colocated)
   int moe0 = 0;
   long long T_max = 0;
+  unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
   XferLayout L{};
   void *local = nullptr;              // this rank's exchange region
   std::vector<void *> peer_base;      // every rank's region (mapped), by rank
   std::vector<void *> opened;         // IPC mappings to close
-  unsigned *counter = nullptr;        // last-block counter (device)
-  int *err = nullptr;                 // wait timeout flag (device)
+  unsigned *counter = nullptr;        // last-block counters [kinds][2 epoch slots] (device)
+  int *err = nullptr;                 // XferErr words (device)
+  int transport = kXferP2P;
+  unsigned long long routed_epoch = 0;  // routed: routing of this epoch already pushed
+  // routed transport, attention side: the step's schedule (K1 over every
+  // shard's routing) and each owned token's destination-instance mask per
+  // epoch slot ([2][ta_max])
+  janus_assignment rws{};
+  uint32_t *dmask = nullptr;
   // NVLS multicast transport (mc.cpp): the bulk rows / routing / partial sums
   // go through one multicast object; flags stay in the IPC regions above.
   bool mc = false, mc_bound = false;
@@ -130,6 +168,7 @@ struct XferState {
   size_t mc_bytes = 0, mc_gran = 0;
   size_t mx_off = 0, mex_off = 0, mgw_off = 0, mpart_off = 0, mslot = 0;  // slot 0; slot 1 = + mslot
 };
+constexpr int kCounterKinds = 2;  // 0: row dispatch, 1: routing push
 
 bool mc_supported(int device);
 std::string mc_create(XferState &x, int device, int *fd);  // rank 0
@@ -137,22 +176,36 @@ std::string mc_join(XferState &x, int device, int fd);     // other ranks
 std::string mc_bind(XferState &x, int device);             // every rank, after all joined
 void mc_free(XferState &x, int device);
 
+inline size_t xfer_slot(unsigned long long epoch) { return (size_t)(epoch & 1); }
+// Attention rank: broadcast dispatch — shard rows (+ routing) into every MoE
+// rank (P2P) or the multicast mapping (NVLS); flag_dispatch.
 cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *d_ex,
                             const float *d_gw, long long T, unsigned long long epoch,
                             cudaStream_t s);
-cudaError_t launch_wait(const XferState &x, bool dispatch_flags, unsigned long long epoch,
-                        cudaStream_t s);
-cudaError_t launch_combine_push(const XferState &x, const void *y, const int32_t *slot_row,
-                                const int32_t *slot_inst, const float *gw, long long T,
-                                unsigned long long epoch, cudaStream_t s);
+// Routed transport, attention rank: shard routing into every rank; flag_route.
+cudaError_t launch_route_push(const XferState &x, const int32_t *d_ex, const float *d_gw,
+                              long long T, unsigned long long epoch, cudaStream_t s);
+// Routed transport, attention rank: each owned row only to the MoE ranks its
+// slots were scheduled on (inst = K1's per-slot instance over the whole step);
+// records the destination masks; flag_dispatch.
+cudaError_t launch_routed_dispatch(const XferState &x, const void *d_x, const int32_t *inst,
+                                   const int32_t *status, long long T, unsigned long long epoch,
+                                   cudaStream_t s);
+// Wait for flags (kind 0 dispatch, 1 combine, 2 route) of `epoch`; the combine
+// wait also collects the MoE ranks' error slots.  Sets err[kErrSkip].
+cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, cudaStream_t s);
+// MoE rank: publish {status} + flag_combine[g] = epoch on every attention rank,
+// after this rank's partial sums landed (P2P push, or its multicast backing).
+cudaError_t launch_signal_combine(const XferState &x, const int32_t *status,
+                                  unsigned long long epoch, cudaStream_t s);
+// Attention rank: out = sum over the MoE partials (P2P / routed: fixed
+// instance order, fp32; NVLS: switch-reduced).
 cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta,
                                    unsigned long long epoch, cudaStream_t s);
-inline size_t xfer_slot(unsigned long long epoch) { return (size_t)(epoch & 1); }
-// multicast path: partial sums already in this MoE rank's backing -> raise the
-// attention ranks' combine flags; attention: switch-reduced read of its rows
-cudaError_t launch_signal_combine(const XferState &x, unsigned long long epoch, cudaStream_t s);
 cudaError_t launch_reduce_mc(const XferState &x, void *d_out, long long first, long long Ta,
                              unsigned long long epoch, cudaStream_t s);
+// K5 in push mode: where the MoE rank's per-token partial sums go.
+PushDst push_dst(const XferState &x, unsigned long long epoch);
 
 }  // namespace janus
 

@@ -6,20 +6,30 @@
 //   * token ownership on the attention side: even split, remainder to the lowest
 //     instance ids (comm.cpp:76-81, janus_shard_tokens);
 //   * gating is MoE-side, so every MoE instance receives every token's full
-//     activation (comm.hpp:12-14; test_comm.cpp:35-64) — here with its routing
-//     (top-k ids) and gate weights, which the scheduler on each MoE GPU needs
-//     (it runs replicated on identical inputs);
+//     activation (comm.hpp:12-14; test_comm.cpp:35-64) — the broadcast
+//     transports (P2P, NVLS) — here with its routing (top-k ids) and gate
+//     weights, which the scheduler on each MoE GPU needs (it runs replicated on
+//     identical inputs);
+//   * routed transport (north_star's "permute into per-GPU buffers"): with the
+//     routing known on the attention side, each attention GPU runs the same K1
+//     over the whole step's routing and sends a row only to the MoE GPUs its
+//     slots were scheduled on — the per-destination traffic StepTraffic counts
+//     (comm.hpp:20-39) restricted to the instances that need the token, as the
+//     one-to-one plan's spread phase does (comm.cpp:155-160).  The layout is
+//     the replicated K1/K2 output, so no count exchange;
 //   * the MoE side's per-token aggregation "plays the all-reduce role" on the
 //     way back (comm.hpp:96-98): each MoE GPU pushes its partial sums for the
-//     tokens an attention GPU owns; the owner adds the M partials in a fixed
-//     instance order.
+//     tokens an attention GPU owns (K5 in push mode, ffn.cu); the owner adds the
+//     partials in a fixed instance order.
 //
 // Transport: every rank allocates one exchange region (identical layout on all
-// ranks, CUDA IPC handle exchanged once); kernels store straight into peers'
-// regions over NVLink (P2P), fused with the copy / combine math, then publish
-// with a system-scope release store of the step's epoch into the receiver's
-// flag.  Receivers wait with acquire loads (bounded: a stuck peer sets an error
-// flag instead of hanging the GPU).
+// ranks, CUDA IPC handle exchanged once, or raw pointers in one process); kernels
+// store straight into peers' regions over NVLink (P2P), fused with the copy /
+// combine math, then publish with a system-scope release store of the step's
+// epoch into the receiver's flag.  Receivers wait with acquire loads (bounded:
+// a stuck peer sets an error word instead of hanging the GPU, and the step's
+// later kernels skip their work).  A failed MoE step (unknown expert) travels
+// to the attention ranks in an error slot written before the combine flag.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -31,7 +41,7 @@ namespace janus {
 namespace {
 
 constexpr int kMaxPeers = 16;
-constexpr unsigned long long kWaitTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+static_assert(kMaxPeers == kPushMaxPeers, "peer tables");
 
 struct PeerPtrs {
   unsigned char *base[kMaxPeers];
@@ -51,23 +61,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// Shard rule (comm.cpp:76-81) on the device.
-__device__ __forceinline__ void shard_of(long long T, int A, long long t, int &a, long long &first) {
-  const long long base = T / A, rem = T % A;
-  const long long big = rem * (base + 1);
-  if (t < big) {
-    a = (int)(t / (base + 1));
-    first = (long long)a * (base + 1);
-  } else {
-    a = (int)(rem + (t - big) / base);
-    first = big + (long long)(a - rem) * base;
-  }
-}
-
 // Grid-wide completion: the last block to finish publishes the flags.
 // Every thread fences its own peer stores (system scope) before the block
 // counts itself done; the last block fences again (acquire side) before it
-// publishes.
+// publishes.  Each kernel kind and epoch slot has its own counter, so kernels
+// of different kinds (or of two steps in flight) never share one.
 __device__ __forceinline__ bool last_block(unsigned *counter) {
   __shared__ bool last;
   __threadfence_system();
@@ -84,9 +82,9 @@ __device__ __forceinline__ bool last_block(unsigned *counter) {
   return last;
 }
 
-// Attention rank `a`: push this shard's rows, routing and gate weights into
-// every MoE rank's receive buffers at the shard's token offset, then raise
-// flag_dispatch[a] = epoch on each MoE rank.
+// Attention rank `a`, broadcast transports: push this shard's rows, routing
+// and gate weights into every MoE rank's receive buffers at the shard's token
+// offset, then raise flag_dispatch[a] = epoch on each MoE rank.
 // Destinations: the M MoE ranks' IPC regions (P2P), or the one multicast
 // mapping (NVLS: the switch replicates each store to every rank).
 struct DispatchDst {
@@ -140,10 +138,91 @@ __global__ void dispatch_kernel(DispatchDst dst, PeerPtrs peers, int M, int moe0
   }
 }
 
+// Routed transport, attention rank `a`: its shard's routing (ids + gate
+// weights, 8 B per slot) into every rank of the box — the MoE ranks schedule
+// and combine with it, the other attention ranks run the same K1 on it — then
+// flag_route[a] = epoch everywhere.
+__global__ void route_push_kernel(PeerPtrs peers, int world, int a, const int32_t *__restrict__ ex,
+                                  const float *__restrict__ gw, long long first, long long ns,
+                                  int k, size_t ex_off, size_t gw_off, XferLayout L,
+                                  unsigned long long epoch, unsigned *counter) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ns; i += stride) {
+    const int32_t e = __ldg(ex + i);
+    const float w = __ldg(gw + i);
+    for (int r = 0; r < world; ++r) {
+      reinterpret_cast<int32_t *>(peers.base[r] + ex_off)[first * k + i] = e;
+      reinterpret_cast<float *>(peers.base[r] + gw_off)[first * k + i] = w;
+    }
+  }
+  if (last_block(counter) && threadIdx.x < world) {
+    unsigned long long *flag =
+        reinterpret_cast<unsigned long long *>(peers.base[threadIdx.x] + L.flag_route_off) + a;
+    st_release_sys(flag, epoch);
+  }
+}
+
+// Routed transport, attention rank `a`: one warp per owned token t.  Lanes
+// j < k read the instance K1 scheduled slot (t, j) on and OR them into t's
+// destination mask; the row is loaded once and stored only into those MoE
+// ranks' receive buffers (at its token position, so the MoE side's permute
+// reads it exactly where a broadcast would have put it).  The mask is kept
+// for the combine.  A rejected step (K1 status) sends nothing but still
+// publishes, so no MoE rank waits for it.
+__global__ void routed_dispatch_kernel(PeerPtrs peers, int M, int moe0, int a,
+                                       const uint4 *__restrict__ x,
+                                       const int32_t *__restrict__ inst,
+                                       const int32_t *__restrict__ status, long long first,
+                                       long long Ta, int vec, int k, size_t x_off,
+                                       uint32_t *__restrict__ dmask, int *err, XferLayout L,
+                                       unsigned long long epoch, unsigned *counter) {
+  const int lane = threadIdx.x & 31;
+  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const bool ok = status == nullptr || status[0] == JANUS_OK;
+  if (!ok && blockIdx.x == 0 && threadIdx.x == 0) {  // this rank's own K1 rejected the step
+    if (atomicCAS(err + kErrStatus, 0, status[0]) == 0) err[kErrBad] = status[1];
+  }
+  constexpr int U = 4;
+  for (long long t = warp0; t < Ta; t += nwarps) {
+    uint32_t bit = 0;
+    for (int j = lane; ok && j < k; j += 32) {
+      const int g = __ldg(inst + (first + t) * k + j);
+      if (g >= 0 && g < 32) bit |= 1u << g;
+    }
+    const uint32_t mask = __reduce_or_sync(0xffffffffu, bit);  // 0: nothing sent, zeros back
+    if (lane == 0) dmask[t] = mask;
+    const uint4 *src = x + t * vec;
+    for (int c0 = lane; mask && c0 < vec; c0 += 32 * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c0 + 32 * u < vec) v[u] = __ldg(src + c0 + 32 * u);
+      for (uint32_t m = mask; m; m &= m - 1) {
+        const int g = __ffs(m) - 1;
+        uint4 *d = reinterpret_cast<uint4 *>(peers.base[moe0 + g] + x_off) + (first + t) * vec;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + 32 * u < vec) d[c0 + 32 * u] = v[u];
+      }
+    }
+  }
+  if (last_block(counter) && threadIdx.x < M) {
+    unsigned long long *flag =
+        reinterpret_cast<unsigned long long *>(peers.base[moe0 + threadIdx.x] + L.flag_dispatch_off) +
+        a;
+    st_release_sys(flag, epoch);
+  }
+}
+
 // Wait until flags[0..n) all reach epoch (one warp).  On timeout, record an
-// error instead of hanging.
+// error instead of hanging.  errs (combine waits): the MoE ranks' {status,
+// bad} slots of this epoch, read after the acquire of the same rank's flag;
+// the first failure is kept (sticky) for janus_xfer_check.  err[kErrSkip]
+// tells the step's later kernels whether to skip.
 __global__ void wait_flags_kernel(const unsigned long long *flags, int n,
-                                  unsigned long long epoch, int *err) {
+                                  unsigned long long epoch, const int2 *errs, int *err, int kind,
+                                  unsigned long long timeout_ns) {
   const int lane = threadIdx.x;
   const unsigned long long t0 = gtimer();
   bool done = false;
@@ -152,59 +231,49 @@ __global__ void wait_flags_kernel(const unsigned long long *flags, int n,
     for (int i = lane; i < n; i += 32) mine = mine && ld_acquire_sys(flags + i) >= epoch;
     done = __all_sync(0xffffffffu, mine);
     if (!done) {
-      if (gtimer() - t0 > kWaitTimeoutNs) {
-        if (lane == 0) atomicExch(err, 1);
+      if (gtimer() - t0 > timeout_ns) {
+        if (lane == 0) {
+          atomicExch(err + kErrTimeout, 1);
+          if (atomicCAS(err + kErrStatus, 0, JANUS_EPEER) == 0) err[kErrBad] = 0;
+          err[kErrSkip + kind] = 1;
+        }
         return;
       }
       __nanosleep(200);
     }
   }
+  int2 mine_err = make_int2(0, 0);
+  if (errs)
+    for (int i = lane; i < n; i += 32) {
+      const unsigned long long u = *reinterpret_cast<const volatile unsigned long long *>(errs + i);
+      const int2 v = make_int2((int)(u & 0xffffffffu), (int)(u >> 32));
+      if (v.x != JANUS_OK && mine_err.x == JANUS_OK) mine_err = v;
+    }
+  const unsigned bad = __ballot_sync(0xffffffffu, mine_err.x != JANUS_OK);
+  if (bad && lane == __ffs(bad) - 1) {
+    if (atomicCAS(err + kErrStatus, 0, mine_err.x) == 0) err[kErrBad] = mine_err.y;
+  }
+  if (lane == 0) err[kErrSkip + kind] = bad ? 1 : 0;
 }
 
-// MoE rank g: partial[t] = sum over this instance's slots of w * y (fixed j
-// order, fp32), stored as bf16 straight into the owning attention rank's
-// part_recv[g][t - first]; then raise flag_combine[g] = epoch there.
-__global__ void combine_push_kernel(PeerPtrs peers, int A, int g, const __nv_bfloat16 *__restrict__ y,
-                                    const int32_t *__restrict__ slot_row,
-                                    const int32_t *__restrict__ slot_inst,
-                                    const float *__restrict__ gw, long long T, int k, int d_h,
-                                    long long ta_max, XferLayout L, size_t part_off,
-                                    unsigned long long epoch, unsigned *counter) {
-  const int vec = d_h / 8;
-  const long long n = T * vec;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long t = idx / vec;
-    const int c = (int)(idx % vec);
-    float acc[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const long long s = t * k + j;
-      if (__ldg(slot_inst + s) != g) continue;
-      const float w = __ldg(gw + s);
-      const uint4 v =
-          __ldg(reinterpret_cast<const uint4 *>(y + (size_t)__ldg(slot_row + s) * d_h) + c);
-      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h[e]);
-        acc[2 * e] += w * f.x;
-        acc[2 * e + 1] += w * f.y;
-      }
-    }
-    uint4 o;
-    __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&o);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
-    int a;
-    long long first;
-    shard_of(T, A, t, a, first);
-    uint4 *dst = reinterpret_cast<uint4 *>(peers.base[a] + part_off) +
-                 ((long long)g * ta_max + (t - first)) * vec;
-    dst[c] = o;
+// MoE rank g: its partial sums of this epoch landed (the K5 push kernel ran
+// before on the stream, or wrote its multicast backing); publish the step's
+// status into every attention rank's error slot, then flag_combine[g] = epoch
+// there.  The release store is cumulative over the preceding kernel's writes
+// (stream order), so the owner's reads see them.
+__global__ void signal_combine_kernel(PeerPtrs peers, int A, int g, XferLayout L, size_t err_off,
+                                      const int32_t *__restrict__ status, int *own_err,
+                                      unsigned long long epoch) {
+  __threadfence_system();
+  const int2 st = status ? make_int2(status[0], status[1]) : make_int2(0, 0);
+  if (threadIdx.x == 0 && st.x != JANUS_OK) {  // keep it on this rank too
+    if (atomicCAS(own_err + kErrStatus, 0, st.x) == 0) own_err[kErrBad] = st.y;
   }
-  if (last_block(counter) && threadIdx.x < A) {
+  if (threadIdx.x < A) {
+    *reinterpret_cast<volatile unsigned long long *>(peers.base[threadIdx.x] + err_off +
+                                                     8 * (size_t)g) =
+        (unsigned long long)(unsigned)st.x | ((unsigned long long)(unsigned)st.y << 32);
+    __threadfence_system();
     unsigned long long *flag =
         reinterpret_cast<unsigned long long *>(peers.base[threadIdx.x] + L.flag_combine_off) + g;
     st_release_sys(flag, epoch);
@@ -212,17 +281,23 @@ __global__ void combine_push_kernel(PeerPtrs peers, int A, int g, const __nv_bfl
 }
 
 // Attention rank: out[t] = sum_g part_recv[g][t] in instance order (fp32).
+// Routed: only the instances in t's destination mask pushed a partial.
+// A failed step (err[kErrSkip]) yields zeros.
 __global__ void reduce_partials_kernel(const __nv_bfloat16 *__restrict__ part, int M,
                                        long long Ta, long long ta_max, int d_h,
+                                       const uint32_t *__restrict__ dmask, const int *skip,
                                        __nv_bfloat16 *__restrict__ out) {
   const int vec = d_h / 8;
   const long long n = Ta * vec;
+  const bool zero = *skip != 0;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
        idx += (long long)gridDim.x * blockDim.x) {
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-    for (int g = 0; g < M; ++g) {
+    uint32_t mask = zero ? 0u : (dmask ? __ldg(dmask + idx / vec) : (M >= 32 ? ~0u : (1u << M) - 1u));
+    for (; mask; mask &= mask - 1) {
+      const int g = __ffs(mask) - 1;
       const uint4 v = reinterpret_cast<const uint4 *>(part + (size_t)g * ta_max * d_h)[idx];
       const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
 #pragma unroll
@@ -240,34 +315,22 @@ __global__ void reduce_partials_kernel(const __nv_bfloat16 *__restrict__ part, i
   }
 }
 
-// MoE rank g (multicast path): its partial sums are already in its own backing
-// (K5 with the instance filter); publish flag_combine[g] = epoch on every
-// attention rank.  The release store is cumulative over the preceding kernel's
-// writes (stream order), so the switch-side reads see them.
-__global__ void signal_combine_kernel(PeerPtrs peers, int A, int g, XferLayout L,
-                                      unsigned long long epoch) {
-  __threadfence_system();
-  if (threadIdx.x < A) {
-    unsigned long long *flag =
-        reinterpret_cast<unsigned long long *>(peers.base[threadIdx.x] + L.flag_combine_off) + g;
-    st_release_sys(flag, epoch);
-  }
-}
-
 // Attention rank (multicast path): out[t] = sum over every rank's backing of
 // part[first + t], reduced by the NVSwitch (multimem.ld_reduce, fp32
 // accumulation, one rounding to bf16).  Ranks that hold no partial for a row
 // contribute zeros.
-__global__ void reduce_mc_kernel(const uint4 *__restrict__ mc_part, long long n,
+__global__ void reduce_mc_kernel(const uint4 *__restrict__ mc_part, long long n, const int *skip,
                                  uint4 *__restrict__ out) {
   constexpr int U = 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
+  const bool zero = *skip != 0;
   for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
     uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const long long i = i0 + u * stride;
-      if (i < n)
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (i < n && !zero)
         asm volatile(
             "multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
             : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
@@ -297,6 +360,16 @@ PeerPtrs peer_ptrs(const XferState &x) {
   return p;
 }
 
+void shard_host(const XferState &x, long long T, long long &first, long long &Ta) {
+  const long long base = T / x.A, rem = T % x.A;
+  Ta = base + (x.rank < rem ? 1 : 0);
+  first = x.rank * base + std::min<long long>(x.rank, rem);
+}
+
+unsigned *counter_for(const XferState &x, int kind, unsigned long long epoch) {
+  return x.counter + 2 * kind + xfer_slot(epoch);
+}
+
 }  // namespace
 
 XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
@@ -308,6 +381,8 @@ XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
   o = up(o + 8 * (size_t)A);
   L.flag_combine_off = o;
   o = up(o + 8 * (size_t)M);
+  L.flag_route_off = o;
+  o = up(o + 8 * (size_t)A);
   const size_t slot0 = o;
   L.x_off = o;
   o = up(o + (size_t)T_max * d_h * 2);
@@ -317,6 +392,8 @@ XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
   o = up(o + (size_t)T_max * k * 4);
   L.part_off = o;
   o = up(o + (size_t)M * ta_max * d_h * 2);
+  L.err_off = o;
+  o = up(o + 8 * (size_t)M);
   L.slot_stride = o - slot0;
   L.bytes = o + L.slot_stride;
   L.ta_max = ta_max;
@@ -326,13 +403,8 @@ XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
 cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *d_ex,
                             const float *d_gw, long long T, unsigned long long epoch,
                             cudaStream_t s) {
-  const int a = x.rank;
   long long first = 0, Ta = 0;
-  {
-    const long long base = T / x.A, rem = T % x.A;
-    Ta = base + (a < rem ? 1 : 0);
-    first = a * base + std::min<long long>(a, rem);
-  }
+  shard_host(x, T, first, Ta);
   const int vec = x.d_h / 8;
   DispatchDst dst{};
   if (x.mc) {  // one store per element; the NVSwitch replicates it to every rank
@@ -351,29 +423,66 @@ cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *
     dst.ex_off = x.L.ex_off + so;
     dst.gw_off = x.L.gw_off + so;
   }
-  dispatch_kernel<<<grid_for(std::max<long long>(Ta * vec, 1)), 256, 0, s>>>(
-      dst, peer_ptrs(x), x.M, x.moe0, a, reinterpret_cast<const uint4 *>(d_x), d_ex, d_gw, first, Ta,
-      vec, x.k, x.L, epoch, x.counter);
+  dispatch_kernel<<<grid_for(std::max<long long>(Ta * x.d_h / 8, 1)), 256, 0, s>>>(
+      dst, peer_ptrs(x), x.M, x.moe0, x.rank, reinterpret_cast<const uint4 *>(d_x), d_ex, d_gw,
+      first, Ta, vec, x.k, x.L, epoch, counter_for(x, 0, epoch));
   return cudaGetLastError();
 }
 
-cudaError_t launch_wait(const XferState &x, bool dispatch_flags, unsigned long long epoch,
-                        cudaStream_t s) {
+cudaError_t launch_route_push(const XferState &x, const int32_t *d_ex, const float *d_gw,
+                              long long T, unsigned long long epoch, cudaStream_t s) {
+  long long first = 0, Ta = 0;
+  shard_host(x, T, first, Ta);
+  const size_t so = xfer_slot(epoch) * x.L.slot_stride;
+  route_push_kernel<<<grid_for(std::max<long long>(Ta * x.k, 1)), 256, 0, s>>>(
+      peer_ptrs(x), x.world, x.rank, d_ex, d_gw, first, Ta * x.k, x.k, x.L.ex_off + so,
+      x.L.gw_off + so, x.L, epoch, counter_for(x, 1, epoch));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_routed_dispatch(const XferState &x, const void *d_x, const int32_t *inst,
+                                   const int32_t *status, long long T, unsigned long long epoch,
+                                   cudaStream_t s) {
+  long long first = 0, Ta = 0;
+  shard_host(x, T, first, Ta);
+  const size_t so = xfer_slot(epoch) * x.L.slot_stride;
+  routed_dispatch_kernel<<<grid_for(std::max<long long>(Ta * 32, 1)), 256, 0, s>>>(
+      peer_ptrs(x), x.M, x.moe0, x.rank, reinterpret_cast<const uint4 *>(d_x), inst, status,
+      first, Ta, x.d_h / 8, x.k, x.L.x_off + so, x.dmask + xfer_slot(epoch) * x.L.ta_max, x.err,
+      x.L, epoch, counter_for(x, 0, epoch));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, cudaStream_t s) {
   unsigned char *base = static_cast<unsigned char *>(x.local);
-  const unsigned long long *flags = reinterpret_cast<const unsigned long long *>(
-      base + (dispatch_flags ? x.L.flag_dispatch_off : x.L.flag_combine_off));
-  wait_flags_kernel<<<1, 32, 0, s>>>(flags, dispatch_flags ? x.A : x.M, epoch, x.err);
+  const size_t off = kind == 0 ? x.L.flag_dispatch_off
+                               : kind == 1 ? x.L.flag_combine_off : x.L.flag_route_off;
+  const int n = kind == 1 ? x.M : x.A;
+  const int2 *errs =
+      kind == 1 ? reinterpret_cast<const int2 *>(base + x.L.err_off + xfer_slot(epoch) * x.L.slot_stride)
+                : nullptr;
+  wait_flags_kernel<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned long long *>(base + off), n,
+                                     epoch, errs, x.err, kind, x.timeout_ns);
   return cudaGetLastError();
 }
 
-cudaError_t launch_combine_push(const XferState &x, const void *y, const int32_t *slot_row,
-                                const int32_t *slot_inst, const float *gw, long long T,
-                                unsigned long long epoch, cudaStream_t s) {
-  const int g = x.rank - x.moe0;
-  combine_push_kernel<<<grid_for(std::max<long long>(T * (x.d_h / 8), 1)), 256, 0, s>>>(
-      peer_ptrs(x), x.A, g, reinterpret_cast<const __nv_bfloat16 *>(y), slot_row, slot_inst, gw,
-      T, x.k, x.d_h, x.L.ta_max, x.L, x.L.part_off + xfer_slot(epoch) * x.L.slot_stride, epoch,
-      x.counter);
+PushDst push_dst(const XferState &x, unsigned long long epoch) {
+  PushDst p{};
+  for (int a = 0; a < x.A && a < kPushMaxPeers; ++a)
+    p.base[a] = static_cast<unsigned char *>(x.peer_base[a]);
+  p.part_off = x.L.part_off + xfer_slot(epoch) * x.L.slot_stride;
+  p.ta_max = x.L.ta_max;
+  p.A = x.A;
+  p.g = x.rank - x.moe0;
+  p.skip_empty = x.transport == kXferRouted ? 1 : 0;
+  return p;
+}
+
+cudaError_t launch_signal_combine(const XferState &x, const int32_t *status,
+                                  unsigned long long epoch, cudaStream_t s) {
+  signal_combine_kernel<<<1, 32, 0, s>>>(peer_ptrs(x), x.A, x.rank - x.moe0, x.L,
+                                         x.L.err_off + xfer_slot(epoch) * x.L.slot_stride, status,
+                                         x.err, epoch);
   return cudaGetLastError();
 }
 
@@ -385,12 +494,8 @@ cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta
       reinterpret_cast<const __nv_bfloat16 *>(base + x.L.part_off +
                                                xfer_slot(epoch) * x.L.slot_stride),
       x.M, Ta, x.L.ta_max, x.d_h,
-      reinterpret_cast<__nv_bfloat16 *>(d_out));
-  return cudaGetLastError();
-}
-
-cudaError_t launch_signal_combine(const XferState &x, unsigned long long epoch, cudaStream_t s) {
-  signal_combine_kernel<<<1, 32, 0, s>>>(peer_ptrs(x), x.A, x.rank - x.moe0, x.L, epoch);
+      x.transport == kXferRouted ? x.dmask + xfer_slot(epoch) * x.L.ta_max : nullptr,
+      x.err + kErrSkip + 1, reinterpret_cast<__nv_bfloat16 *>(d_out));
   return cudaGetLastError();
 }
 
@@ -401,7 +506,8 @@ cudaError_t launch_reduce_mc(const XferState &x, void *d_out, long long first, l
   const uint4 *part =
       reinterpret_cast<const uint4 *>(x.mc_va + x.mpart_off + xfer_slot(epoch) * x.mslot) +
       first * vec;
-  reduce_mc_kernel<<<grid_for((n + 3) / 4), 256, 0, s>>>(part, n, reinterpret_cast<uint4 *>(d_out));
+  reduce_mc_kernel<<<grid_for((n + 3) / 4), 256, 0, s>>>(part, n, x.err + kErrSkip + 1,
+                                                          reinterpret_cast<uint4 *>(d_out));
   return cudaGetLastError();
 }
 

@@ -22,8 +22,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
-from ._lib import OK, lib
-from .moesim import JanusError, shard_tokens
+from ._lib import EUNKNOWN_EXPERT, OK, lib
+from .moesim import JanusError, ValidationError, shard_tokens
 
 
 @dataclass(frozen=True)
@@ -91,7 +91,8 @@ class BoxPlan:
 
 
 class _Ctx:
-    """A bare device context (attention ranks hold no replica map)."""
+    """A bare device context (attention ranks of a broadcast box hold no
+    replica map; the routed transport gives them one, see JanusBox)."""
 
     def __init__(self, device: int):
         self.ctx = C.c_void_p()
@@ -102,16 +103,37 @@ class _Ctx:
     def last_error(self) -> str:
         return lib.janus_last_error(self.ctx).decode()
 
+    def __del__(self):
+        try:
+            if self.ctx:
+                lib.janus_destroy(self.ctx)
+        except Exception:
+            pass
+
+
+TRANSPORTS = ("auto", "p2p", "nvls", "routed")
+
 
 class JanusBox:
     """This rank's endpoint of the box exchange.
 
     For an MoE rank pass ``layer`` (a :class:`paper_2512_13525_b200.moe.MoELayer`
-    built with ``instance = rank - n_attn`` and its weight store set)."""
+    built with ``instance = rank - n_attn`` and its weight store set).
+    ``transport``: ``p2p`` / ``nvls`` broadcast every token to every MoE rank
+    (the reference's semantics, comm.hpp:12-14); ``routed`` sends a row only to
+    the MoE ranks its slots are scheduled on — attention ranks then also need
+    the replica map (``rmap``) to run the scheduler; ``auto`` = NVLS when every
+    rank supports it, else P2P.
+
+    Multi-process (one rank per GPU): the constructor exchanges the CUDA IPC
+    handles over torch.distributed.  One process driving every rank (e.g. all on
+    one GPU): :meth:`local`."""
 
     def __init__(self, plan: BoxPlan, rank: int, max_tokens: int, d_hidden: int, top_k: int,
-                 layer=None, device: int = 0, group=None, transport: str = "auto"):
-        import torch.distributed as dist
+                 layer=None, device: int = 0, group=None, transport: str = "auto", rmap=None,
+                 _connect: bool = True):
+        if transport not in TRANSPORTS:
+            raise ValueError(transport)
         self.plan, self.rank = plan, rank
         self.max_tokens, self.d_h, self.k = max_tokens, d_hidden, top_k
         if plan.is_moe(rank):
@@ -122,7 +144,13 @@ class JanusBox:
             self._err = layer.sched.last_error
         else:
             self.layer = None
-            self._c = _Ctx(device)
+            if transport == "routed":  # the attention rank schedules the step too
+                if rmap is None:
+                    raise ValueError("the routed transport needs the replica map on attention ranks")
+                from .moesim import Scheduler
+                self._c = Scheduler(rmap, device)
+            else:
+                self._c = _Ctx(device)
             self._ctx = self._c.ctx
             self._err = self._c.last_error
         if plan.colocated:
@@ -131,16 +159,19 @@ class JanusBox:
         else:
             self._check(lib.janus_xfer_configure(self._ctx, plan.n_attn, plan.n_moe, rank,
                                                  max_tokens, d_hidden, top_k))
+        self.transport = "routed" if transport == "routed" else "p2p"
+        if transport == "routed":
+            self._check(lib.janus_xfer_set_transport(self._ctx, 1))
+        if not _connect:
+            return
+        import torch.distributed as dist
         h = C.create_string_buffer(64)
         self._check(lib.janus_xfer_handle(self._ctx, h))
         handles = [None] * plan.world
         dist.all_gather_object(handles, bytes(h.raw), group=group)
         self._check(lib.janus_xfer_connect(self._ctx, b"".join(handles)))
         dist.barrier(group=group)
-        self.transport = "p2p"
-        if transport not in ("auto", "p2p", "nvls"):
-            raise ValueError(transport)
-        if transport != "p2p":
+        if transport in ("auto", "nvls"):
             yes = C.c_int()
             self._check(lib.janus_xfer_mc_supported(self._ctx, C.byref(yes)))
             every = [None] * plan.world
@@ -150,6 +181,26 @@ class JanusBox:
                 self.transport = "nvls"
             elif transport == "nvls":
                 raise JanusError(5, "xfer: NVLS multicast not supported on every rank")
+
+    @classmethod
+    def local(cls, plan: BoxPlan, max_tokens: int, d_hidden: int, top_k: int, layers: dict,
+              devices=None, transport: str = "p2p", rmap=None) -> list:
+        """Every rank's endpoint in this process (``layers``: rank -> MoELayer
+        of the MoE ranks; ``devices``: rank -> device, default 0), connected
+        with raw pointers (janus_xfer_connect_local).  P2P or routed transport.
+        Calls into ranks that wait on one another must be enqueued in causal
+        order (e.g. on one stream: every dispatch, then every MoE step, then
+        every combine)."""
+        if transport not in ("p2p", "routed"):
+            raise ValueError("a same-process box uses the p2p or routed transport")
+        devices = devices or {}
+        boxes = [cls(plan, r, max_tokens, d_hidden, top_k, layer=layers.get(r),
+                     device=devices.get(r, 0), transport=transport, rmap=rmap, _connect=False)
+                 for r in range(plan.world)]
+        arr = (C.c_void_p * plan.world)(*[b._ctx.value for b in boxes])
+        for b in boxes:
+            b._check(lib.janus_xfer_connect_local(b._ctx, arr))
+        return boxes
 
     def _setup_multicast(self, dist, group) -> None:
         """Rank 0 creates the multicast object; its POSIX fd reaches the other
@@ -191,7 +242,28 @@ class JanusBox:
         if st != OK:
             raise JanusError(st, self._err())
 
+    def _check_status(self, st):
+        if st == EUNKNOWN_EXPERT:
+            raise ValidationError(self._err())
+        self._check(st)
+
+    def set_timeout(self, seconds: float) -> None:
+        self._check(lib.janus_xfer_set_timeout(self._ctx, int(seconds * 1e9)))
+
+    def check(self) -> None:
+        """Raise the first failed step this rank saw since the last check: the
+        reference's ValidationError for an unknown expert (on the attention
+        side, reported by any MoE rank), JanusError(EPEER) for a peer that
+        never published."""
+        self._check_status(lib.janus_xfer_check(self._ctx))
+
     # --- attention rank ------------------------------------------------------
+    def route(self, experts_shard, gate_w_shard, num_tokens: int, epoch: int,
+              stream: int) -> None:
+        """Routed transport: push the routing phase ahead of :meth:`dispatch`."""
+        self._check(lib.janus_attn_route_async(self._ctx, experts_shard.data_ptr(),
+                                               gate_w_shard.data_ptr(), num_tokens, epoch, stream))
+
     def dispatch(self, x_shard, experts_shard, gate_w_shard, num_tokens: int, epoch: int,
                  stream: int) -> None:
         """experts / gate_w None: rows only, the MoE ranks gate (set_router)."""
@@ -208,6 +280,18 @@ class JanusBox:
     # --- MoE rank ---------------------------------------------------------------
     def moe_step(self, num_tokens: int, epoch: int, stream: int) -> None:
         self._check(lib.janus_moe_layer_xfer_async(self._ctx, num_tokens, epoch, stream))
+
+    def recv_rows(self, epoch: int, num_tokens: int):
+        """This rank's receive buffer of token rows for ``epoch``'s slot as an
+        int16 torch view [num_tokens, d_h] (instrumentation: tests)."""
+        import torch
+        ptr = C.c_void_p()
+        self._check(lib.janus_xfer_recv_rows(self._ctx, epoch, C.byref(ptr)))
+
+        class _Dev:  # __cuda_array_interface__ over the exchange region
+            __cuda_array_interface__ = {"data": (ptr.value, False), "typestr": "<i2",
+                                        "shape": (num_tokens, self.d_h), "version": 3}
+        return torch.as_tensor(_Dev(), device="cuda")
 
     def timed_out(self) -> bool:
         v = C.c_int()

@@ -1,7 +1,9 @@
 """Multi-GPU worker for tests/test_gpu_dist.py (launched with torchrun, one rank
 per GPU).  Runs several decode steps of an A-attention + M-MoE box through the
-C-ABI exchange and checks every attention shard's output against the same
-layer computed on one GPU (instance -1, all replicas local).
+C-ABI exchange and checks every attention shard's output against the fp32
+oracle (oracle.c or_expert_swiglu + the combine sum, tests/_ffn_ref.py) — with
+h rounded as the device rounds it (2^-6 rel + 2^-6 rms) and pure fp32
+(2^-5 rel + 2^-5 rms) — and every rank's janus_xfer_check.
 
   torchrun --nproc-per-node A+M tests/dist_worker.py --attn A --moe M --out DIR
 """
@@ -16,12 +18,17 @@ import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import paper_2512_13525_b200 as J  # noqa: E402
 from paper_2512_13525_b200.dist import BoxPlan, JanusBox  # noqa: E402
 from paper_2512_13525_b200.moe import MoELayer, build_weight_store, make_inputs  # noqa: E402
+from _ffn_ref import err_stats, moe_reference, u16  # noqa: E402
+from oracle import Oracle  # noqa: E402
 
-RTOL = ATOL = 2.0 ** -6
+RTOL = ATOL = 2.0 ** -6          # vs the oracle with h rounded like the device
+RTOL32 = ATOL32 = 2.0 ** -5      # vs the pure fp32 oracle
 
 
 def main():
@@ -31,7 +38,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=300)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out")
-    ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls"])
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls", "routed"])
     ap.add_argument("--shared", action="store_true", help="add a shared expert (NVLS only)")
     ap.add_argument("--shared-split", action="store_true",
                     help="the shared expert split evenly over the MoE instances (implies --shared)")
@@ -70,24 +77,26 @@ def main():
         wr = router_weights(E, d_h, 13, dev)
         if layer is not None:
             layer.set_router(wr)
-    box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local, transport=args.transport)
-    full = None
-    if att:
-        full = MoELayer(rmap, d_h, d_e, T, k, instance=-1, device=local)
-        full.set_weights(*build_weight_store(full, seed=1))
-        if args.shared:
-            full.set_shared(*shared_w)
-        if args.gate:
-            full.set_router(wr)
+    box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local, transport=args.transport,
+                   rmap=rmap)
+    orc = Oracle()
+    from paper_2512_13525_b200.moe import expert_weights
+    wcache = {}
+
+    def weights_of(e):
+        if e not in wcache:
+            wcache[e] = tuple(u16(w) for w in (expert_weights(99, d_h, d_e, 5, dev) if e == -1
+                                               else expert_weights(e, d_h, d_e, 1, dev)))
+        return wcache[e]
 
     stream = torch.cuda.current_stream(dev).cuda_stream
     result = {"rank": rank, "role": plan.role(rank), "steps": [], "transport": box.transport}
     steps = []
     for step in range(1, args.steps + 1):
         Ts = T - 37 * (step % 3)  # vary the step size: ragged shards
-        b = J.gen_batch(J.RoutingPattern.gaussian(E, 0.2), Ts, k, 7, step)
+        _, cdf = orc.pattern("gaussian", E, sigma=0.2)
         x, gw = make_inputs(Ts, k, d_h, step, dev)
-        ex = torch.from_numpy(b.experts).to(dev)
+        ex = torch.from_numpy(orc.gen_batch(cdf, Ts, k, 7, step)).to(dev)
         steps.append((Ts, x, gw, ex))
 
     outs = {}
@@ -136,14 +145,37 @@ def main():
             result["steps"].append({"T": Ts})
             continue
         first, cnt = plan.shard(Ts, rank)
-        ref = (full.forward_gated(x) if args.gate else full.forward(x, ex, gw))[first:first + cnt]
-        torch.cuda.synchronize()
-        o, r = outs[step].float().cpu().numpy(), ref.float().cpu().numpy()
-        rms = float(np.sqrt(np.mean(r.astype(np.float64) ** 2))) or 1.0
-        bad = int((np.abs(o - r) > RTOL * np.abs(r) + ATOL * rms).sum())
-        result["steps"].append({"T": Ts, "shard": [first, cnt], "bad": bad,
-                                "max_err_over_rms": float(np.abs(o - r).max() / rms)})
+        xs = u16(x[first:first + cnt])
+        keep = np.ones(cnt, bool)
+        if args.gate:  # the routing the MoE ranks computed: the gating oracle on the same rows
+            exn, wn, lg = orc.gate(xs, u16(wr), k, want_logits=True)
+            exn, wn = exn.reshape(cnt, k), wn.reshape(cnt, k)
+            srt = -np.sort(-lg, axis=1)  # tokens whose k-th / (k+1)-th logits nearly tie
+            keep = srt[:, k - 1] - srt[:, k] > 1e-3  # may select differently (fp32 vs double)
+        else:
+            exn = ex.cpu().numpy().reshape(Ts, k)[first:first + cnt]
+            wn = gw.cpu().numpy().reshape(Ts, k)[first:first + cnt]
+        if args.shared:  # the shared expert: one more slot of weight 1 on every token
+            exn = np.concatenate([exn, np.full((cnt, 1), -1, np.int32)], axis=1)
+            wn = np.concatenate([wn, np.ones((cnt, 1), np.float32)], axis=1)
+        o = outs[step][:cnt].float().cpu().numpy()[keep]
+        xs, exn, wn = xs[keep], exn[keep], wn[keep]
+        bad = n32 = 0
+        errs = [0.0, 0.0]
+        for i, (rh, tol_r, tol_a) in enumerate(((True, RTOL, ATOL), (False, RTOL32, ATOL32))):
+            r = moe_reference(orc, xs, exn, wn, weights_of, round_h=rh)
+            rms = float(np.sqrt(np.mean(r.astype(np.float64) ** 2))) or 1.0
+            nb = int((np.abs(o - r) > tol_r * np.abs(r) + tol_a * rms).sum())
+            bad, n32 = (nb, n32) if rh else (bad, nb)
+            errs[i] = err_stats(o, r)[0]
+        result["steps"].append({"T": Ts, "shard": [first, cnt], "bad": bad + n32,
+                                "max_err_over_rms": errs[0], "max_err_over_rms_fp32": errs[1]})
     result["timed_out"] = box.timed_out()
+    try:
+        box.check()
+        result["check"] = "ok"
+    except Exception as ex_:  # noqa: BLE001
+        result["check"] = str(ex_)
     os.makedirs(args.out, exist_ok=True)
     with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}{'x' if args.shared_split else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}_rank{rank}.json"), "w") as f:
         json.dump(result, f)

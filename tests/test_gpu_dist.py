@@ -18,7 +18,8 @@ def gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("transport,inflight", [("p2p", 1), ("p2p", 2), ("nvls", 1), ("nvls", 2)])
+@pytest.mark.parametrize("transport,inflight", [("p2p", 1), ("p2p", 2), ("nvls", 1), ("nvls", 2),
+                                               ("routed", 1), ("routed", 2)])
 @pytest.mark.parametrize("attn,moe", [(1, 1), (1, 3), (2, 2)])
 def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
     if gpus() < attn + moe:
@@ -26,7 +27,8 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
     out = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={attn + moe}", "--master-addr", "127.0.0.1", "--master-port",
-           str(29500 + 10 * attn + moe + (50 if transport == "nvls" else 0) + 100 * inflight),
+           str(29500 + 10 * attn + moe + {"p2p": 0, "nvls": 50, "routed": 300}[transport] +
+               100 * inflight),
            os.path.join(ROOT, "tests", "dist_worker.py"),
            "--attn", str(attn), "--moe", str(moe), "--out", out, "--transport", transport,
            "--inflight", str(inflight)]
@@ -36,6 +38,7 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
     assert len(res) == attn + moe
     for r in res:
         assert not r["timed_out"], r
+        assert r["check"] == "ok", r
         assert r["transport"] == transport
         if r["role"] in ("attention", "both"):
             for s in r["steps"]:
@@ -69,7 +72,7 @@ def test_box_exchange_shared_expert_and_moe_side_gating(flag):
                 assert s_["bad"] == 0, s_
 
 
-@pytest.mark.parametrize("n,transport", [(2, "nvls"), (4, "nvls"), (4, "p2p")])
+@pytest.mark.parametrize("n,transport", [(2, "nvls"), (4, "nvls"), (4, "p2p"), (4, "routed")])
 def test_moe_only_colocated_box(n, transport):
     """The MoE-only box (every rank owns a shard and is an MoE instance), two
     steps in flight."""
@@ -78,7 +81,8 @@ def test_moe_only_colocated_box(n, transport):
     out = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
-           str(29800 + 10 * n + (transport == "p2p")), os.path.join(ROOT, "tests", "dist_worker.py"),
+           str(29800 + 10 * n + {"nvls": 0, "p2p": 1, "routed": 2}[transport]),
+           os.path.join(ROOT, "tests", "dist_worker.py"),
            "--attn", str(n), "--moe", str(n), "--out", out, "--transport", transport,
            "--inflight", "2", "--colocated"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
