@@ -6,18 +6,27 @@ Contract (see task spec): one JSON line on rank 0.
 Workload (BASELINE.json configs[1], "c2"): Qwen3-30B-A3B-shaped MoE layer —
 128 experts, top-8, d_h=2048, d_e=768, SwiGLU, bf16 random-init weights, the
 committed c2 replica map (N=1, reference placement pipeline), Zipf(1.0)
-routing from gen_batch (seed 0x30).  One step = one MoE layer over one batch of
-T tokens: K1 schedule + K3 permute + K4 grouped GEMMs + K5 combine.  The
-weight store (1.21 GB) is far larger than L2, so every step streams it from HBM.
+routing from the reference's own gen_batch (oracle/_ref; seed 0x30).  One step
+= one MoE layer over one batch of T tokens: K1 schedule + K3 permute + K4
+grouped GEMMs + K5 combine.  The weight store (1.21 GB) is far larger than L2,
+so every step streams it from HBM.
 
-Under torchrun (N > 1) every rank runs the same single-GPU layer on its own
-batch ("replicas", weak scaling) — the attention->MoE split lives in
-paper_2512_13525_b200/dist.py and bench_dist.py.
+Under torchrun (N > 1) the ranks form one NVLink box (BoxPlan.for_gpus: 1A+1E,
+1A+3E, 2A+6E): attention GPUs dispatch their token shards to the MoE GPUs and
+combine the partial sums.  ``value`` is then the whole box's
+tokens/s divided by ALL N GPUs (per-GPU, as the metric says); the per-MoE-GPU
+figure is a side field.
 
-``--impl reference`` times the reference's CPU path on the host cores: the
-reference's own schedule() (oracle/_ref, compiled from /root/reference) plus
-the oracle's fp32 SwiGLU expert FFN (the reference has no FFN), on a bounded
-sample of the same workload.
+Input generation (routing batches) is test infrastructure — the reference's
+gen_batch through oracle/_ref, or the pinned oracle restatement — and runs
+outside every timed region.
+
+``--impl reference`` times the reference's CPU path on the host cores without
+importing this package: the reference's own schedule() and
+schedule_reference() (oracle/_ref, compiled from /root/reference) on the same
+batches, plus a CPU SwiGLU FFN from the build's parity oracle (the reference
+has no FFN; labelled "build_oracle"), and the reference's moe_layer_latency
+model (latency.cpp:17-32) beside it, labelled modelled.
 """
 from __future__ import annotations
 
@@ -148,63 +157,143 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_sample(T, tokens_sample, batches, layer_experts_w, nthreads):
-    """Time the reference CPU path on a bounded sample: reference schedule() on
-    the full batch + oracle fp32 SwiGLU FFN for `tokens_sample` tokens' rows."""
+def oracle_mod():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import CSRMap, Oracle, Ref
+    import oracle
+    return oracle
 
-    import paper_2512_13525_b200 as J
-    ref, orc = Ref(), Oracle()
-    rm, _ = shape_map(J, 1)
-    m = CSRMap(rm.num_experts, rm.num_instances, rm.slots_per_instance, *rm.csr())
-    b0 = batches[0]
-    t_sched = ref.time_schedule(np.concatenate(batches), T, K_TOP, m, "schedule", reps=21) * 1e-6
-    t_sched_ref = ref.time_schedule(np.concatenate(batches), T, K_TOP, m, "reference",
-                                    reps=21) * 1e-6
-    ex = b0.reshape(T, K_TOP)[:tokens_sample]
+
+def gen_batches(T, n=N_BATCHES, E_=None, s=1.0, seed=None, k=None):
+    """Routing batches (input generation, never timed): the reference's own
+    gen_batch from_pmf(1/(e+1)^s) (oracle/_ref) when built, else the pinned
+    oracle restatement (bit-identical, tests/test_oracle_vs_ref.py)."""
+    o = oracle_mod()
+    E_ = E if E_ is None else E_
+    k = K_TOP if k is None else k
+    seed = SEED if seed is None else seed
+    w = np.array([1.0 / (e + 1) ** s for e in range(E_)])
+    try:
+        ref = o.Ref()
+        return [ref.gen_batch("pmf", E_, T, k, seed, T * 1000 + i, weights=w) for i in range(n)]
+    except FileNotFoundError:
+        orc = o.Oracle()
+        _, cdf = orc.pattern("pmf", E_, weights=w)
+        return [orc.gen_batch(cdf, T, k, seed, T * 1000 + i) for i in range(n)]
+
+
+def csr_map(name):
+    """A committed config map as the oracle's CSRMap (no product import)."""
+    o = oracle_mod()
+    return o.CSRMap.from_map_text(open(os.path.join(ROOT, "paper_2512_13525_b200", "maps",
+                                                   f"{name}.map")).read())
+
+
+def map_name(M):
+    if MAP == "c2":
+        return "c2" if M == 1 else f"c2_m{M}"
+    if MAP == "c3":
+        return f"c3_m{M}"
+    return None if M == 1 else f"c4_n{M}"
+
+
+def cpu_map(M=1):
+    o = oracle_mod()
+    name = map_name(M)
+    if name is None:  # c4 on one GPU: every expert local
+        return o.CSRMap.from_lists(1, E, [[0]] * E)
+    return csr_map(name)
+
+
+def cpu_weights_fn():
+    """Deterministic CPU-side bf16 expert weights for the CPU sample (numbers
+    only need the right shape)."""
+    o = oracle_mod()
+    orc = o.Oracle()
+    cache = {}
+
+    def fn(e):
+        if e not in cache:
+            r = np.random.default_rng(e)
+            cache[e] = tuple(orc.f32_to_bf16(r.standard_normal(sh).astype(np.float32) * sc)
+                             for sh, sc in (((D_E, D_H), D_H ** -0.5), ((D_E, D_H), D_H ** -0.5),
+                                            ((D_H, D_E), D_E ** -0.5)))
+        return cache[e]
+    return fn
+
+
+def cpu_sample(T, tokens_sample, batches, wfn, nthreads, hbm, tf_sus):
+    """The CPU side of the path on a bounded sample, every piece labelled:
+      * the reference's schedule() (4-thread OMP team as shipped) and
+        schedule_reference() (1 core) on the full batches — oracle/_ref;
+      * a CPU SwiGLU FFN for `tokens_sample` tokens' top-k rows — the build's
+        parity oracle (the reference has no FFN): kind "build_oracle";
+      * the reference's moe_layer_latency model (latency.cpp:17-32) on the
+        same schedule at the measured B200 peaks: kind "modelled".
+    Returns the composite tokens/s (reference schedule() + build-oracle FFN,
+    pro-rated to the sample) and the components."""
+    o = oracle_mod()
+    ref, orc = o.Ref(), o.Oracle()
+    m = cpu_map(1)
+    allb = np.concatenate(batches)
+    t_sched = ref.time_schedule(allb, T, K_TOP, m, "schedule", reps=21) * 1e-6
+    t_sched_ref = ref.time_schedule(allb, T, K_TOP, m, "reference", reps=21) * 1e-6
+    a0 = ref.schedule(batches[0], T, K_TOP, m, "schedule")
+    # the model as shipped (2 matrices) at the measured peaks, t_launch 5 us
+    t_model = ref.moe_layer_latency(a0.load, a0.routed_tokens, D_H, D_E, 2, tf_sus * 1e12,
+                                    hbm * 1e9, 5e-6)
+    ex = batches[0].reshape(T, K_TOP)[:tokens_sample]
     by_e = {}
     for t in range(tokens_sample):
         for j in range(K_TOP):
             by_e.setdefault(int(ex[t, j]), []).append(t)
     rng = np.random.default_rng(0)
-    x = rng.standard_normal((tokens_sample, D_H)).astype(np.float32)
-    xu = orc.f32_to_bf16(x)
-    ws_ = {e: layer_experts_w(e) for e in by_e}  # weight generation outside the timing
+    xu = orc.f32_to_bf16(rng.standard_normal((tokens_sample, D_H)).astype(np.float32))
+    ws_ = {e: wfn(e) for e in by_e}  # weight generation outside the timing
     t0 = time.perf_counter()
     for e, toks in by_e.items():
         wg, wu, wd = ws_[e]
         orc.expert_swiglu(xu[toks], wg, wu, wd, round_h=True, nthreads=nthreads)
     t_ffn = time.perf_counter() - t0
     t_step_sample = t_ffn + t_sched * tokens_sample / T
+    comp = [
+        {"name": "schedule()", "kind": "reference", "source": "oracle/_ref (aebs.cpp:172-197)",
+         "us_per_call": t_sched * 1e6, "cores": 4, "tokens": T},
+        {"name": "schedule_reference()", "kind": "reference",
+         "source": "oracle/_ref (aebs.cpp:199-248)", "us_per_call": t_sched_ref * 1e6, "cores": 1,
+         "tokens": T},
+        {"name": "fp32 SwiGLU expert FFN", "kind": "build_oracle",
+         "source": "oracle/oracle.c or_expert_swiglu (build oracle, not reference: the "
+                   "reference has no FFN)", "seconds": t_ffn, "cores": nthreads,
+         "tokens": tokens_sample, "tokens_per_s": tokens_sample / t_ffn},
+        {"name": "moe_layer_latency", "kind": "modelled",
+         "source": "oracle/_ref latency.cpp:17-32 at the measured peaks (HBM "
+                   f"{hbm:.1f} GB/s, bf16 {tf_sus:.1f} TFLOP/s), t_launch 5 us; 2 matrices, "
+                   "2 FLOP per (token, d_h, d_e) as shipped",
+         "us_per_layer": t_model * 1e6, "tokens_per_s": T / t_model},
+    ]
     return {"tok_s": tokens_sample / t_step_sample, "t_sched_us": t_sched * 1e6,
-            "t_sched_reference_us": t_sched_ref * 1e6, "t_ffn_s": t_ffn,
+            "t_sched_reference_us": t_sched_ref * 1e6, "components": comp,
             "sample_tokens": tokens_sample}
 
 
-def cpu_weights_fn():
-    """Deterministic CPU-side bf16 expert weights for the CPU sample (the CPU
-    arm has no GPU; numbers only need the right shape)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import Oracle
-    orc = Oracle()
-    cache = {}
-
-    def fn(e):
-        if e not in cache:
-            r = np.random.default_rng(e)
-            cache[e] = tuple(orc.f32_to_bf16(r.standard_normal(s).astype(np.float32) * sc)
-                             for s, sc in (((D_E, D_H), D_H ** -0.5), ((D_E, D_H), D_H ** -0.5),
-                                           ((D_H, D_E), D_E ** -0.5)))
-        return cache[e]
-    return fn
-
-
-def gen_batches(T):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import paper_2512_13525_b200 as J
-    pat = J.RoutingPattern.zipf(E, 1.0)
-    return [J.gen_batch(pat, T, K_TOP, SEED, T * 1000 + i).experts for i in range(N_BATCHES)]
+def c5_scheduler_cpu(tokens=(32, 256, 4096)):
+    """BASELINE c5 (E=256, N=6, Zipf 1.2, seed 0x5A): the reference's
+    schedule() / schedule_reference() µs and AEBS vs random max-load, on the
+    host cores (oracle/_ref)."""
+    o = oracle_mod()
+    ref = o.Ref()
+    m = csr_map("c5")
+    rows = {}
+    for T in tokens:
+        b = gen_batches(T, 1, 256, 1.2, 0x5A)[0]
+        a = ref.schedule(b, T, 8, m, "schedule")
+        r = ref.schedule(b, T, 8, m, "random", seed=7)
+        rows[T] = {"cpu_schedule_us": ref.time_schedule(b, T, 8, m, "schedule", reps=101),
+                   "cpu_schedule_reference_us": ref.time_schedule(b, T, 8, m, "reference",
+                                                                  reps=101),
+                   "max_load_aebs": int(a.load.max()), "max_load_random": int(r.load.max()),
+                   "batch": b}
+    return rows
 
 
 def run_reference(args):
@@ -215,29 +304,34 @@ def run_reference(args):
     batches = gen_batches(T)
     nthreads = os.cpu_count() or 1
     wfn = cpu_weights_fn()
+    hbm, tf_burst, tf_sus, src = peaks()
     sample = max(1, min(T, args.cpu_sample_tokens))
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(T, sample, batches, wfn, nthreads)
+        r = cpu_sample(T, sample, batches, wfn, nthreads, hbm, tf_sus or tf_burst)
         if i >= args.warmup:
             vals.append(r)
     tok_s = float(np.median([v["tok_s"] for v in vals]))
+    c5 = c5_scheduler_cpu()
     line = {
         "impl": "reference", "metric": "moe_layer_tokens_per_s_per_gpu", "value": tok_s,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic", "config": workload_config(T, args),
-        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": nthreads,
-                         "kind": "reference",
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": nthreads, "kind": "port",
                          "sample": f"reference schedule() (oracle/_ref, 4-thread OMP team as "
-                                   f"shipped) on the full T={T} batch, pro-rated, + fp32 SwiGLU "
-                                   f"FFN (oracle port; reference has none) for {sample} tokens "
-                                   f"x top-8 rows on {nthreads} threads"},
+                                   f"shipped) on the full T={T} batch, pro-rated, + the build "
+                                   f"oracle's fp32 SwiGLU FFN (the reference has no FFN) for "
+                                   f"{sample} tokens x top-8 rows on {nthreads} threads",
+                         "components": vals[-1]["components"]},
         "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "scheduler": {"cpu_schedule_us": float(np.median([v["t_sched_us"] for v in vals])),
                       "cpu_schedule_reference_us": float(np.median(
-                          [v["t_sched_reference_us"] for v in vals]))},
+                          [v["t_sched_reference_us"] for v in vals])),
+                      "c5": {str(t): {k_: v_ for k_, v_ in r.items() if k_ != "batch"}
+                             for t, r in c5.items()}},
+        "imports_product": "paper_2512_13525_b200" in sys.modules,
     }
     print(json.dumps(line), flush=True)
 
@@ -371,7 +465,11 @@ def run_ours(args):
     flops_avg = float(np.mean([alg_flops[i % N_BATCHES] for i in range(args.steps)]))
     gbs = bytes_avg / ffn_s / 1e9
     tfs = flops_avg / ffn_s / 1e12
-    hbm_bound = gbs / hbm >= tfs / (tf_sus or tf_burst)
+    # tensor peak: the burst figure for a short timed region, the sustained
+    # (power-capped) one for a run long enough to settle (B200_PROFILING.md)
+    tf_peak, tf_which = ((tf_burst, "burst") if ms / 1e3 < 2.0 or not tf_sus
+                         else (tf_sus, "sustained"))
+    hbm_bound = gbs / hbm >= tfs / tf_peak
     # DRAM bytes of the two grouped GEMMs from the committed ncu --set full
     # capture of this workload (profiles/r1/ncu_traffic.json), per step like
     # `achieved`'s bytes; null for shapes / sizes not captured
@@ -382,8 +480,8 @@ def run_ours(args):
         traffic = tr["grouped_gemm_dram_bytes_per_step"] if tr else None
     roofline = ({"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                  "traffic": traffic} if hbm_bound else
-                {"bound": "tensor", "achieved": tfs, "peak": tf_sus or tf_burst,
-                 "unit": "TFLOP/s", "frac": tfs / (tf_sus or tf_burst), "traffic": traffic})
+                {"bound": "tensor", "achieved": tfs, "peak": tf_peak,
+                 "unit": "TFLOP/s", "frac": tfs / tf_peak, "traffic": traffic})
     roofline["traffic_unit"] = "DRAM bytes per step (ncu), vs alg_bytes_per_step"
     roofline.update({"kernel": "grouped_gemm_kernel (gate-up SwiGLU + down), per layer call",
                      "peak_source": f"{src} (MEASURED_PEAKS.json)",
@@ -394,29 +492,48 @@ def run_ours(args):
                             "of the same steps launched without the CUDA graph",
                      "ms_per_step_without_graph": ms_nograph / args.steps,
                      "alg_bytes_per_step": bytes_avg, "alg_flops_per_step": flops_avg,
-                     "hbm_frac": gbs / hbm, "tensor_frac": tfs / (tf_sus or tf_burst)})
+                     "hbm_frac": gbs / hbm, "tensor_frac": tfs / tf_peak,
+                     "tensor_peak": f"{tf_which} bf16 {tf_peak} TFLOP/s (timed region "
+                                    f"{ms / 1e3:.2f} s)"})
     if rank != 0:
         dist.destroy_process_group() if ws > 1 else None
         return
 
     cpu = None
+    cpu_sched = (None, None)
+    c5 = {}
     if not args.no_cpu:
         try:
             r = cpu_sample(T, max(1, min(T, args.cpu_sample_tokens)), gen_batches(T),
-                           cpu_weights_fn(), os.cpu_count() or 1)
+                           cpu_weights_fn(), os.cpu_count() or 1, hbm, tf_sus or tf_burst)
             cpu = {"value": r["tok_s"], "unit": "tokens/s", "cores": os.cpu_count() or 1,
-                   "kind": "reference",
+                   "kind": "port",
                    "sample": f"reference schedule() (oracle/_ref) on the full batch, pro-rated, "
-                             f"+ oracle fp32 SwiGLU FFN for {r['sample_tokens']} tokens "
-                             f"(x top-8 rows); reference schedule() {r['t_sched_us']:.1f} us, "
-                             f"schedule_reference() {r['t_sched_reference_us']:.1f} us"}
+                             f"+ the build oracle's fp32 SwiGLU FFN (the reference has no FFN) "
+                             f"for {r['sample_tokens']} tokens (x top-8 rows)",
+                   "components": r["components"]}
             cpu_sched = (r["t_sched_us"], r["t_sched_reference_us"])
+            c5 = c5_scheduler_cpu()
         except Exception as ex:  # oracle/_ref missing on this box
-            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
+            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port",
                    "sample": f"unavailable: {ex}"}
-            cpu_sched = (None, None)
-    else:
-        cpu_sched = (None, None)
+    # BASELINE c5 (E=256, N=6, Zipf 1.2): the GPU scheduler on the same batches
+    # as the CPU numbers, and the AEBS vs random max-activated-experts/GPU
+    c5_line = {}
+    if c5:
+        s5 = J.Scheduler(J.config_map("c5"), local)
+        for t5, r5 in c5.items():
+            d5 = torch.from_numpy(r5["batch"]).to(dev)
+            b5 = J.ActivationBatch(t5, 8, r5["batch"])
+            c5_line[str(t5)] = {
+                "gpu_us_per_iter": s5.time_schedule(d5, t5, 8, reps=51),
+                "cpu_schedule_us": r5["cpu_schedule_us"],
+                "cpu_schedule_reference_us": r5["cpu_schedule_reference_us"],
+                "max_load_aebs": s5.schedule(b5).max_load(),
+                "max_load_random": s5.schedule_random(b5, 7).max_load(),
+                "cpu_max_load_aebs": r5["max_load_aebs"],
+                "cpu_max_load_random": r5["max_load_random"]}
+        s5.close()
 
     line = {
         "metric": "moe_layer_tokens_per_s_per_gpu", "value": value, "unit": "tokens/s",
@@ -426,7 +543,8 @@ def run_ours(args):
         "config": workload_config(T, args),
         "tokens_per_s_per_gpu": value / ws,
         "scheduler": {"us_per_iter": sched_us, "how": "CUDA-graph replay of 20 passes, median",
-                      "cpu_schedule_us": cpu_sched[0], "cpu_schedule_reference_us": cpu_sched[1]},
+                      "cpu_schedule_us": cpu_sched[0], "cpu_schedule_reference_us": cpu_sched[1],
+                      "c5": c5_line},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "tokens/s",
@@ -474,10 +592,8 @@ def run_box(args):
             from paper_2512_13525_b200.moe import router_weights
             layer.set_router(router_weights(E, D_H, 13, dev))
     box = JanusBox(plan, rank, T, D_H, K_TOP, layer=layer, device=local,
-                   transport=args.transport)
-    pat = J.RoutingPattern.zipf(E, 1.0)
-    batches = [torch.from_numpy(J.gen_batch(pat, T, K_TOP, SEED, T * 1000 + i).experts).to(dev)
-               for i in range(N_BATCHES)]
+                   transport=args.transport, rmap=shape_map(J, M)[0])
+    batches = [torch.from_numpy(b).to(dev) for b in gen_batches(T)]
     x, gw = make_inputs(T, K_TOP, D_H, 3, dev)
     first, cnt = plan.shard(T, rank) if att else (0, 0)
     xs = x[first:first + cnt].contiguous()
@@ -669,13 +785,14 @@ def run_box(args):
     e2e_s = float(tt.item())
     timed_out = box.timed_out()
     if rank == 0:
-        value = T * args.steps / (ms_max / 1e3)
+        box_tok_s = T * args.steps / (ms_max / 1e3)
+        value = box_tok_s / ws  # per GPU of the box (all N, attention GPUs included)
         sends = plan.bytes_per_step(T, D_H, 0 if args.gate else K_TOP)
         send_bytes = sends[0][0]
         hbm, tf_burst, tf_sus, src = peaks()
         gbs_slow = alg_slow / (ffn_ms / 1e3) / 1e9 if ffn_ms > 0 else 0.0
         tfs_slow = algf_slow / (ffn_ms / 1e3) / 1e12 if ffn_ms > 0 else 0.0
-        tf_peak = tf_sus or tf_burst
+        tf_peak = tf_burst if ms_max / 1e3 < 2.0 or not tf_sus else tf_sus
         hbm_bound = gbs_slow / hbm >= tfs_slow / tf_peak
         roof = ({"bound": "hbm", "achieved": gbs_slow, "peak": hbm, "unit": "GB/s",
                  "frac": gbs_slow / hbm} if hbm_bound else
@@ -707,7 +824,9 @@ def run_box(args):
                                  "attention-side: top-k ids and gate weights shipped with "
                                  "the rows",
                        "l2": "inputs > L2 (weights streamed)"},
-            "tokens_per_s_per_gpu": value / ws, "tokens_per_s_per_moe_gpu": value / M,
+            "tokens_per_s_box": box_tok_s, "tokens_per_s_per_moe_gpu": box_tok_s / M,
+            "value_is": "whole-box tokens/s / N GPUs (attention GPUs included; they run no "
+                        "attention math here)",
             "roofline": {**roof, "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
                          "ffn_us_per_step": ffn_ms * 1e3,
                          "traffic": None, "alg_bytes_per_step": alg_slow,
@@ -733,7 +852,7 @@ def run_box(args):
                        / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else None,
                        "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy "
                                                          "per direction (fallback)"},
-            "e2e": {"value": T * args.steps / e2e_s, "unit": "tokens/s",
+            "e2e": {"value": T * args.steps / e2e_s / ws, "unit": "tokens/s",
                     "h2d_bytes_per_step": T * (D_H * 2 + (0 if args.gate else K_TOP * 8)),
                     "d2h_bytes_per_step": T * D_H * 2},
             "scheduler": {"us_per_iter": sched_us, "slots": T * K_TOP,
@@ -764,8 +883,9 @@ def main():
     ap.add_argument("--gate", action="store_true",
                     help="box: MoE-side gating (rows only cross NVLink; every MoE GPU runs "
                          "the router GEMM + top-k on the full step)")
-    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls"],
-                    help="box exchange for --gpus > 1 (auto: NVLS multicast when supported)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls", "routed"],
+                    help="box exchange for --gpus > 1 (auto: NVLS multicast when supported; "
+                         "routed: rows only to the MoE GPUs their slots are scheduled on)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     apply_shape(args.shape)

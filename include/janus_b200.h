@@ -18,7 +18,6 @@
  *   janus_moe_layer[_async]<- moe_layer_latency's subject: the MoE layer the
  *                             reference only models (src/latency.cpp:17-32)
  *   janus_moe_layer_latency<- moesim::moe_layer_latency (latency.hpp:34-35)
- *   janus_gen_batch        <- moesim::gen_batch (include/moesim/workload.hpp:31-32)
  *   janus_shard_tokens     <- StepTraffic token ownership (src/comm.cpp:76-81)
  * See INTEGRATION.md for the binding a maintainer adds on the reference side.
  */
@@ -165,7 +164,9 @@ janus_status janus_profile(janus_ctx *ctx, int enable);
 janus_status janus_profile_read(janus_ctx *ctx, double *sched_ms, double *ffn_ms, int *calls);
 /* One scheduler pass over a device batch with in-kernel phase timestamps
  * (%globaltimer, ns): ns[0..6] = start, loads issued + map staged, pass 1,
- * scan + pins, sequential greedy, finish + scans, pass 2. */
+ * scan + pins, sequential greedy, finish + scans, pass 2; ns[7] = SM clock
+ * cycles of the pass where recorded (the decode-size kernel), else 0.
+ * ns has 8 entries. */
 janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int num_tokens,
                                   int top_k, int64_t *ns);
 
@@ -298,10 +299,9 @@ double janus_moe_layer_latency(int num_instances, const int32_t *load,
                                const int64_t *routed_tokens, int d_hidden, int d_expert,
                                int bytes_per_param, double peak_flops, double hbm_bandwidth,
                                double t_launch);
-/* Synthetic routing exactly as gen_batch (workload.cpp:56-130) from an
- * inclusive cdf of num_experts doubles (RoutingPattern::cdf). */
-janus_status janus_gen_batch(const double *cdf, int num_experts, int num_tokens, int top_k,
-                             uint64_t seed, uint64_t step, int32_t *out);
+/* derive_seed (rng.hpp:34-44): the seed of schedule_random and of the
+ * synthetic weights.  (Synthetic routing, gen_batch, is test infrastructure:
+ * oracle/routing.py — not part of this library.) */
 uint64_t janus_derive_seed(uint64_t root, const char *label, uint64_t extra);
 
 #ifdef __cplusplus

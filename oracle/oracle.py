@@ -62,6 +62,35 @@ class CSRMap:
             rids_arr = np.array([r for rr in rids for r in rr], np.int32)
         return CSRMap(len(hosts), N, C, off, flat_h, rids_arr)
 
+    @staticmethod
+    def from_map_text(text: str) -> "CSRMap":
+        """The committed config maps (``paper_2512_13525_b200/maps/*.map``):
+        the reference replica-map text format (aebs.cpp:381-449) with explicit
+        physical ids ``e: g:rid ...``, or dealt ids ``e: g ...`` (aebs.cpp:437-446).
+        Test/bench infrastructure: lets the bench's reference arm read the maps
+        without importing the product."""
+        N = C_ = 0
+        rows = {}
+        for raw in text.splitlines():
+            s = raw.split("#", 1)[0].strip()
+            if not s:
+                continue
+            if "=" in s and (":" not in s or s.index("=") < s.index(":")):
+                key, val = (x.strip() for x in s.split("=", 1))
+                if key == "instances":
+                    N = int(val)
+                elif key == "slots_per_instance":
+                    C_ = int(val)
+                continue
+            e, rest = s.split(":", 1)
+            rows[int(e)] = sorted((int(t.split(":")[0]), int(t.split(":")[1]) if ":" in t else None)
+                                  for t in rest.split())
+        hosts = [[g for g, _ in rows[e]] for e in range(len(rows))]
+        rids = [[r for _, r in rows[e]] for e in range(len(rows))]
+        if any(r is None for rr in rids for r in rr):
+            return CSRMap.from_lists(N, C_, hosts)
+        return CSRMap.from_lists(N, C_, hosts, rids)
+
     def hosts_of(self, e):
         return self.hosts[self.off[e]:self.off[e + 1]]
 

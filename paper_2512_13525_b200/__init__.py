@@ -6,8 +6,8 @@ C++ ``moesim::schedule`` shim, :mod:`.moesim` the Python mirror.  All compute
 runs in ``libjanus_b200.so`` (sm_100a); there is no CPU fallback.
 """
 from .moesim import (ActivationBatch, Assignment, InstanceLoad, ParseError,  # noqa: F401
-                     ReplicaMap, RoutingPattern, Scheduler, ValidationError, config_map,
-                     derive_seed, dump_assignment, gen_batch, load_batch, load_replica_map,
+                     ReplicaMap, Scheduler, ValidationError, config_map,
+                     derive_seed, dump_assignment, load_batch, load_replica_map,
                      load_replica_map_file, max_activated_load, moe_layer_latency, schedule,
                      schedule_random, schedule_reference, shard_tokens)
 

@@ -23,7 +23,7 @@ SYMBOLS = (
     "janus_set_replica_map", "janus_replica_order", "janus_schedule_async", "janus_schedule",
     "janus_time_schedule", "janus_moe_configure", "janus_moe_set_weights",
     "janus_moe_layer_async", "janus_moe_layer", "janus_shard_tokens",
-    "janus_moe_layer_latency", "janus_gen_batch", "janus_derive_seed", "janus_profile",
+    "janus_moe_layer_latency", "janus_derive_seed", "janus_profile",
     "janus_profile_read", "janus_trace_schedule", "janus_xfer_configure", "janus_xfer_handle",
     "janus_xfer_connect", "janus_attn_dispatch_async", "janus_moe_layer_xfer_async",
     "janus_attn_combine_async", "janus_xfer_status", "janus_xfer_mc_supported",
@@ -71,7 +71,6 @@ def _load() -> C.CDLL:
     L.janus_shard_tokens.restype = None
     L.janus_moe_layer_latency.argtypes = [i32, vp, vp, i32, i32, i32, dbl, dbl, dbl]
     L.janus_moe_layer_latency.restype = dbl
-    L.janus_gen_batch.argtypes = [vp, i32, i32, i32, u64, u64, vp]
     L.janus_derive_seed.argtypes = [u64, C.c_char_p, u64]
     L.janus_derive_seed.restype = u64
     L.janus_profile.argtypes = [vp, i32]

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libjanus_b200.so")
-SOURCES = ["api.cu", "aebs.cu", "gemm.cu", "ffn.cu", "xfer.cu", "gate.cu", "stats.cu", "mc.cpp", "workload.cpp"]
+SOURCES = ["api.cu", "aebs.cu", "gemm.cu", "ffn.cu", "xfer.cu", "gate.cu", "stats.cu", "mc.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -26,10 +26,9 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fopenmp", "-Xptxas", "-v" if verbose else "-O3",
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
            f"-I{os.path.join(ROOT, 'include')}", "-o", LIB,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-lgomp"]
+           *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

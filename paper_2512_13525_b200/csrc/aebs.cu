@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -93,10 +94,11 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// Exclusive scan of two int arrays of n entries in place (1024 threads).
+// Exclusive scan of two int arrays of n entries in place (NT threads).
+template <int NT = kSchedThreads>
 __device__ void block_exscan2(int32_t *a, int32_t *b, int n, int32_t *scratch) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int per = (n + kSchedThreads - 1) / kSchedThreads;
+  const int per = (n + NT - 1) / NT;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   int sa = 0, sb = 0;
   for (int i = lo; i < hi; ++i) {
@@ -118,7 +120,7 @@ __device__ void block_exscan2(int32_t *a, int32_t *b, int n, int32_t *scratch) {
   }
   __syncthreads();
   if (warp == 0) {
-    int wa = scratch[lane], wb = scratch[32 + lane];
+    int wa = lane < NT / 32 ? scratch[lane] : 0, wb = lane < NT / 32 ? scratch[32 + lane] : 0;
     int xa = wa, xb = wb;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -198,12 +200,12 @@ struct Slots<0> {
 // Called by every thread of one CTA.
 __device__ void write_error_layout(const SchedArgs &a, int status, int bad) {
   const int R = a.map.R;
-  for (int q = threadIdx.x; q <= R; q += kSchedThreads) {
+  for (int q = threadIdx.x; q <= R; q += blockDim.x) {
     if (a.out.group_off) a.out.group_off[q] = 0;
     if (a.tile_off) a.tile_off[q] = 0;
   }
   if (a.shared_off && threadIdx.x < 4) a.shared_off[threadIdx.x] = 0;
-  for (int s = threadIdx.x; s < a.S; s += kSchedThreads) a.out.instance[s] = -1;
+  for (int s = threadIdx.x; s < a.S; s += blockDim.x) a.out.instance[s] = -1;
   if (threadIdx.x == 0) {
     a.out.status[0] = status;
     a.out.status[1] = bad;
@@ -246,6 +248,16 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   int32_t *s_rid = s_hosts + R;                                 // [R]
   int32_t *s_qidx = s_rid + R;                                  // [R]
   uint32_t *s_hm = reinterpret_cast<uint32_t *>(s_qidx + R);    // [E]
+  // the one-lane pairs greedy's records and list (N <= 8, DevMap::pair_info)
+  const bool pairs = a.map.pair_info != nullptr;
+  const int E4 = (E + 3) & ~3;
+  uint4 *s_pinfo = reinterpret_cast<uint4 *>(
+      (reinterpret_cast<uintptr_t>(s_hm + E) + 15) & ~uintptr_t(15));  // [E]
+  uint4 *s_plist = s_pinfo + E;                                       // [E+4]
+  uint32_t *s_pbhi = reinterpret_cast<uint32_t *>(s_plist + E + 4);   // [E4]
+  uint32_t *s_pbh_list = s_pbhi + E4;                                 // [E4+4]
+  int32_t *s_elist = reinterpret_cast<int32_t *>(s_pbh_list + E4 + 4);  // [E4]
+  int32_t *s_res = s_elist + E4;                                      // [E4+4]
   __shared__ int32_t s_bad;
   __shared__ int32_t s_scan[64];
 
@@ -257,17 +269,56 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   const int beg = min(cend, cbeg + warp * nit * 32), end = min(cend, beg + nit * 32);
   Slots<MAXIT> sl;
   sl.load(a.experts, beg, end, lane, nit);
-  for (int i = tid; i <= E; i += kSchedThreads) s_off[i] = a.map.off[i];
-  for (int i = tid; i < R; i += kSchedThreads) {
+  {
+    // the first element per thread of every map table: all loads go out
+    // before any smem store (in order, a load -> store pair per table would
+    // cost one L2 round trip each)
+    int r_off = 0, r_h = 0, r_r = 0, r_q = 0;
+    uint32_t r_hm = 0, r_pb = 0;
+    uint4 r_pi = make_uint4(0, 0, 0, 0);
+    if (tid <= E) r_off = __ldg(a.map.off + tid);
+    if (tid < R) {
+      r_h = __ldg(a.map.hosts + tid);
+      r_r = __ldg(a.map.rid + tid);
+      r_q = __ldg(a.map.qidx + tid);
+    }
+    if (tid < E) {
+      r_hm = __ldg(a.map.hmask + tid);
+      if (pairs) {
+        r_pi = __ldg(a.map.pair_info + tid);
+        r_pb = __ldg(a.map.pair_bhi + tid);
+      }
+    }
+    for (int i = tid; i < 32 * E; i += kSchedThreads) cnt[i] = 0;
+    if (tid <= E) s_off[tid] = r_off;
+    if (tid < R) {
+      s_hosts[tid] = r_h;
+      s_rid[tid] = r_r;
+      s_qidx[tid] = r_q;
+    }
+    if (tid < E) {
+      s_hm[tid] = r_hm;
+      chg[tid] = -1;
+      if (pairs) {
+        s_pinfo[tid] = r_pi;
+        s_pbhi[tid] = r_pb;
+      }
+    }
+  }
+  for (int i = tid + kSchedThreads; i <= E; i += kSchedThreads) s_off[i] = a.map.off[i];
+  for (int i = tid + kSchedThreads; i < R; i += kSchedThreads) {
     s_hosts[i] = a.map.hosts[i];
     s_rid[i] = a.map.rid[i];
     s_qidx[i] = a.map.qidx[i];
   }
-  for (int e = tid; e < E; e += kSchedThreads) {
+  for (int e = tid + kSchedThreads; e < E; e += kSchedThreads) {
     s_hm[e] = a.map.hmask[e];
     chg[e] = -1;
+    if (pairs) {
+      s_pinfo[e] = __ldg(a.map.pair_info + e);
+      s_pbhi[e] = __ldg(a.map.pair_bhi + e);
+    }
   }
-  for (int i = tid; i < 32 * E; i += kSchedThreads) cnt[i] = 0;
   for (int g = tid; g < N; g += kSchedThreads) {
     load[g] = 0;
     routed[g] = 0;
@@ -340,14 +391,23 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   __syncthreads();
 
   // ---- pins (aebs.cpp:180-185) ------------------------------------------------
-  for (int e = tid; e < E; e += kSchedThreads) {
-    const int r = s_off[e + 1] - s_off[e];
+  for (int e0 = warp * 32; e0 < E; e0 += kSchedThreads) {  // warp-uniform trip count
+    const int e = e0 + lane;
+    const int r = e < E ? s_off[e + 1] - s_off[e] : 0;
+    const bool act = e < E && tot[e] > 0;
     // a validated map gives every expert a replica; the reference's second
     // check (:164-166) is kept for completeness
-    if (tot[e] > 0 && r == 0) atomicMin(&s_bad, e);
-    if (tot[e] > 0 && r == 1) {
-      const int g = s_hosts[s_off[e]];
-      chg[e] = g;
+    if (act && r == 0) atomicMin(&s_bad, e);
+    const bool pin = act && r == 1;
+    const int g = pin ? s_hosts[s_off[e]] : -1;
+    if (pin) chg[e] = g;
+    if (N <= 32) {  // count the pins per instance with one vote per instance, not per expert
+      const unsigned pm = __ballot_sync(kFull, pin);
+      if (pm) {
+        const unsigned my = __match_any_sync(kFull, g);
+        if (pin && lane == __ffs(my & pm) - 1) atomicAdd(&load[g], __popc(my & pm));
+      }
+    } else if (pin) {
       atomicAdd(&load[g], 1);
     }
   }
@@ -362,7 +422,16 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   // ---- sequential phase, warp 0 --------------------------------------------
   if (warp == 0) {
     if (a.policy == JANUS_POLICY_AEBS) {
-      if (N <= 32) {
+      if (pairs) {
+        greedy_pairs(
+            lane, (E + 31) / 32, N, a.map.pairs_only != 0,
+            [&](int w) {
+              const int e = w * 32 + lane;
+              return __ballot_sync(kFull, e < E && tot[e] > 0 && s_off[e + 1] - s_off[e] > 1);
+            },
+            [&](int e) { return s_hm[e]; }, load, s_pinfo, s_pbhi, s_plist, s_pbh_list, s_elist,
+            s_res, chg, load);
+      } else if (N <= 32) {
         greedy_warp(E, N, tot, s_off, s_hm, load, chg);
       } else {
         for (int e = 0; e < E; ++e) {
@@ -478,6 +547,472 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   cluster_wait();
 }
 
+// ---------------------------------------------------------------------------
+// The decode-size scheduler: S <= kSmallMaxSlots slots, N <= 32 instances,
+// R <= kSmallMaxReplicas — one CTA of 16 warps, no cluster, no DSMEM, the map
+// read as compact tables (DevMap::ex_info / rep_info / multi_mask / pin_mask,
+// ~8 B per expert and replica) in the same round trip as the batch.  The
+// order-dependent greedy (aebs.cpp:186-194) starts right after the histogram
+// pass: it needs only the activated set (a bitmask built in pass 1) and the
+// single-replica pins per instance (popc of activated & pin_mask[g]), so warp
+// 0 runs it while the other 15 warps scan the per-warp counts (token totals
+// and each warp's starting rank per expert).  Same outputs, bit for bit, as
+// aebs_schedule_kernel.
+constexpr int kSmallThreads = 512, kSmallWarps = kSmallThreads / 32, kSmallMaxIt = 4;
+constexpr int kSmallMaxSlots = kSmallWarps * kSmallMaxIt * 32;  // 2048
+constexpr int kSmallMaxReplicas = 2048;
+
+__host__ __device__ inline size_t small_absent_off(int E, int N, int R) {
+  const int W = (E + 31) / 32;
+  const size_t b = (size_t)16 * E + (size_t)8 * R + (size_t)4 * kSmallWarps * E + (size_t)16 * E +
+                   (size_t)8 * (R + 1) + (size_t)4 * (2 * W + 2 * N * W) + (size_t)4 * (N + 1);
+  return (b + 15) & ~(size_t)15;
+}
+
+// finish_assignment (aebs.cpp:94-108) for one expert placed on instance g.
+__device__ __forceinline__ void finish_multi(const SchedArgs &a, int e, int g, int4 x,
+                                             const int2 *rep, const int32_t *tot, int32_t *chg,
+                                             int32_t *ridof, int32_t *qof, int32_t *qcnt,
+                                             int32_t *tcnt) {
+  const int t = tot[e];
+  const int p = x.x + __popc((uint32_t)x.z & ((1u << g) - 1u));
+  const int2 rq = rep[p];
+  chg[e] = g;
+  ridof[e] = rq.x;
+  qof[e] = rq.y;
+  qcnt[rq.y] = t;
+  tcnt[rq.y] = a.merge_tail ? max(1, t / a.tile_n) : (t + a.tile_n - 1) / a.tile_n;
+  a.out.expert_instance[e] = g;
+  if (a.out.expert_tokens) a.out.expert_tokens[e] = t;
+}
+
+// The one-lane greedy for N <= 8 instances with loads < 256 (DevMap::pair_info),
+// run by one warp.  The loads live as bytes of two registers (lo: instances
+// 0-3, hi: 4-7).  The activated multi-replica experts are first listed in
+// ascending order with their precomputed records (warp-cooperative, one
+// 32-expert word per round), padded with no-op records to a multiple of 4.
+// One lane then walks the list four records per load round.  For a two-replica
+// expert (hosts a < b) two PRMTs build words equal but for their top byte,
+// load[a] resp. load[b], so one unsigned <= picks a on ties
+// (aebs.cpp:186-194: least-loaded host, ties to the lowest id); the winner's
+// byte gets + 1: a 4-deep dependent chain per expert.  Three or more
+// replicas: a scan of the host bytes (strict <, ascending ids).
+// act_multi(w): word w of the activated multi-replica experts; hmask_of(e):
+// host bitmask; init_load: the pins' loads; results in chg[] and load_out[].
+template <class ActMulti, class HostMask>
+__device__ void greedy_pairs(int lane, int W, int N, bool pairs_only, ActMulti act_multi,
+                             HostMask hmask_of, const int32_t *init_load, const uint4 *pinfo,
+                             const uint32_t *pinfo_bhi, uint4 *plist, uint32_t *pb_hi,
+                             int32_t *elist, int32_t *res, int32_t *chg, int32_t *load_out) {
+  int total = 0;
+  for (int w = 0; w < W; ++w) {
+    const unsigned m = act_multi(w);
+    if ((m >> lane) & 1u) {
+      const int pos = total + __popc(m & lanemask_lt());
+      const int e = w * 32 + lane;
+      const uint4 r = pinfo[e];
+      plist[pos] = make_uint4(r.x, r.y, r.z, r.w);
+      pb_hi[pos] = pinfo_bhi[e];  // read back as uint4 per group of 4
+      elist[pos] = e;
+    }
+    total += __popc(m);
+  }
+  const int padded = (total + 3) & ~3;
+  if (total + lane < padded) {  // no-op records: nothing moves
+    plist[total + lane] = make_uint4(0, 0, 0, 0);
+    pb_hi[total + lane] = 0;
+  }
+  uint32_t lo = 0, hi = 0;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const uint32_t v = (uint32_t)(g < N ? init_load[g] : 0) & 0xffu;
+    if (g < 4)
+      lo |= v << (8 * g);
+    else
+      hi |= v << (8 * (g - 4));
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (pairs_only) {
+      // every multi-replica expert has exactly two hosts: no branch per step
+      for (int i = 0; i < padded; i += 4) {
+        uint4 r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r[u] = plist[i + u];
+        const uint4 bh = *reinterpret_cast<const uint4 *>(pb_hi + i);  // one vector load
+        const uint32_t bhs[4] = {bh.x, bh.y, bh.z, bh.w};
+        int4 out;
+        int *o = reinterpret_cast<int *>(&out);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t da, db;
+          asm("prmt.b32 %0, %1, %2, %3;" : "=r"(da) : "r"(lo), "r"(hi), "r"(r[u].x));
+          asm("prmt.b32 %0, %1, %2, %3;" : "=r"(db) : "r"(lo), "r"(hi), "r"(r[u].x >> 16));
+          const uint32_t keep_a = da <= db ? 0xffffffffu : 0u;
+          lo += r[u].w ^ ((r[u].y ^ r[u].w) & keep_a);  // unconditional uses: no sunk loads
+          hi += bhs[u] ^ ((r[u].z ^ bhs[u]) & keep_a);
+          o[u] = (int)(keep_a & 1u);
+        }
+        *reinterpret_cast<int4 *>(res + i) = out;
+      }
+    } else {
+      for (int i = 0; i < padded; ++i) {
+        const uint4 r = plist[i];
+        int ca;
+        if (r.x != 0xffffffffu) {
+          uint32_t da, db;
+          asm("prmt.b32 %0, %1, %2, %3;" : "=r"(da) : "r"(lo), "r"(hi), "r"(r.x));
+          asm("prmt.b32 %0, %1, %2, %3;" : "=r"(db) : "r"(lo), "r"(hi), "r"(r.x >> 16));
+          ca = da <= db;
+          lo += ca ? r.y : r.w;
+          hi += ca ? r.z : pb_hi[i];
+        } else {  // >= 3 replicas: r.y = host bitmask; ca = the winner
+          uint32_t best = 0xffffffffu;
+          ca = 0;
+          for (uint32_t hm = r.y; hm; hm &= hm - 1) {
+            const int h = __ffs(hm) - 1;
+            uint32_t l;
+            asm("prmt.b32 %0, %1, %2, %3;" : "=r"(l) : "r"(lo), "r"(hi), "r"(h));
+            l &= 0xffu;
+            if (l < best) {
+              best = l;
+              ca = h;
+            }
+          }
+          const uint32_t inc = 1u << (8 * (ca & 3));
+          lo += ca < 4 ? inc : 0u;
+          hi += ca < 4 ? 0u : inc;
+        }
+        res[i] = ca;
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (g < N) {
+        uint32_t l;
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(l) : "r"(lo), "r"(hi), "r"(g));
+        load_out[g] = (int)(l & 0xffu);
+      }
+  }
+  __syncwarp();
+  for (int i = lane; i < total; i += 32) {  // results -> finish, in parallel
+    const int e = elist[i];
+    const uint32_t hm = hmask_of(e);
+    const int rr = res[i];
+    // two replicas: rr = 1 -> the lower host (a), 0 -> b; else rr = the host
+    chg[e] = __popc(hm) == 2 ? (rr ? __ffs(hm) - 1 : 31 - __clz(hm)) : rr;
+  }
+}
+
+// Peers with a compile-time id width (fully unrolled; NB == 0: runtime width).
+template <int NB>
+__device__ __forceinline__ unsigned peers_nb(unsigned valid, int id, int nbits) {
+  if (NB == 0) return peers_of(valid, id, nbits);
+  unsigned peers = valid;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const bool bit = (id >> b) & 1;
+    const unsigned m = __ballot_sync(kFull, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kSmallThreads, 1) aebs_small_kernel(SchedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int E = a.map.E, N = a.map.N, R = a.map.R, S = a.S, W = (E + 31) / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long c0 = 0;
+  if (a.trace && tid == 0) {
+    a.trace[0] = globaltimer();
+    c0 = clock64();
+  }
+  if (a.abort_flag && *a.abort_flag) {  // the box exchange aborted this step
+    write_error_layout(a, JANUS_EPEER, 0);
+    return;
+  }
+  int4 *exi = reinterpret_cast<int4 *>(smem);                   // [E]
+  int2 *rep = reinterpret_cast<int2 *>(exi + E);                // [R]
+  int32_t *cnt = reinterpret_cast<int32_t *>(rep + R);          // [16][E]
+  int32_t *tot = cnt + kSmallWarps * E;                         // [E]
+  int32_t *chg = tot + E;                                       // [E]
+  int32_t *qof = chg + E;                                       // [E]
+  int32_t *ridof = qof + E;                                     // [E]
+  int32_t *qcnt = ridof + E;                                    // [R+1]
+  int32_t *tcnt = qcnt + R + 1;                                 // [R+1]
+  uint32_t *act = reinterpret_cast<uint32_t *>(tcnt + R + 1);   // [W]
+  uint32_t *multi = act + W;                                    // [W]
+  uint32_t *pin = multi + W;                                    // [N][W]
+  uint32_t *hmk = pin + N * W;                                  // [N][W]
+  int32_t *qb = reinterpret_cast<int32_t *>(hmk + N * W);       // [N+1]
+  // pair-record list of the one-lane greedy: [E+1] records, [E] expert ids, and
+  // the per-expert records staged from DevMap::pair_info
+  uint4 *pinfo = reinterpret_cast<uint4 *>(smem + small_absent_off(E, N, R));  // [E]
+  uint4 *plist = pinfo + E;                                     // [E+4]
+  uint32_t *pinfo_bhi = reinterpret_cast<uint32_t *>(plist + E + 4);  // [E]
+  uint32_t *pb_hi = pinfo_bhi + ((E + 3) & ~3);                 // [E+4], 16-B aligned
+  int32_t *elist = reinterpret_cast<int32_t *>(pb_hi + ((E + 3) & ~3) + 4);  // [E]
+  int32_t *res = elist + ((E + 3) & ~3);                        // [E+4], 16-B aligned
+  unsigned char *seen = reinterpret_cast<unsigned char *>(res + E + 4);  // [E]
+  __shared__ int32_t s_load[32];
+  __shared__ int32_t s_bad;
+
+  // ---- one round trip: this warp's slots + the compact map tables ---------
+  const int per = ((S + kSmallWarps - 1) / kSmallWarps + 31) / 32 * 32;
+  const int beg = min(S, warp * per), end = min(S, beg + per);
+  const int nit = (end - beg + 31) / 32;
+  int v[kSmallMaxIt];
+#pragma unroll
+  for (int i = 0; i < kSmallMaxIt; ++i) {
+    const int sl = beg + i * 32 + lane;
+    v[i] = (i < nit && sl < end) ? __ldg(a.experts + sl) : 0;
+  }
+  // Every global load of the first element per thread goes out before any
+  // smem store: an in-order warp would otherwise stall on each load -> store
+  // pair in turn (one L2 round trip per table instead of one in all).
+  const bool pairs = a.map.pair_info != nullptr;
+  int4 r_exi = make_int4(0, 0, 0, 0);
+  int2 r_rep = make_int2(0, 0);
+  uint4 r_pi = make_uint4(0, 0, 0, 0);
+  uint32_t r_pbh = 0, r_multi = 0, r_pin = 0, r_hmk = 0;
+  int r_qb = 0;
+  if (tid < E) r_exi = __ldg(a.map.ex_info + tid);
+  if (tid < R) r_rep = __ldg(a.map.rep_info + tid);
+  if (pairs && tid < E) {
+    r_pi = __ldg(a.map.pair_info + tid);
+    r_pbh = __ldg(a.map.pair_bhi + tid);
+  }
+  if (tid < W) r_multi = __ldg(a.map.multi_mask + tid);
+  if (tid < N * W) {
+    r_pin = __ldg(a.map.pin_mask + tid);
+    r_hmk = __ldg(a.map.host_mask + tid);
+  }
+  if (tid <= N) r_qb = __ldg(a.map.qbase + tid);
+  // zeroing meanwhile
+  for (int i = tid; i < kSmallWarps * E; i += kSmallThreads) cnt[i] = 0;
+  for (int e = tid; e < E; e += kSmallThreads) seen[e] = 0;
+  for (int q = tid; q <= R; q += kSmallThreads) {
+    qcnt[q] = 0;
+    tcnt[q] = 0;
+  }
+  if (tid < E) exi[tid] = r_exi;
+  if (tid < R) rep[tid] = r_rep;
+  if (pairs && tid < E) {
+    pinfo[tid] = r_pi;
+    pinfo_bhi[tid] = r_pbh;
+  }
+  if (tid < W) multi[tid] = r_multi;
+  if (tid < N * W) {
+    pin[tid] = r_pin;
+    hmk[tid] = r_hmk;
+  }
+  if (tid <= N) qb[tid] = r_qb;
+  // tables longer than one element per thread (E or R above 512, N*W above 512)
+  for (int e = tid + kSmallThreads; e < E; e += kSmallThreads) {
+    exi[e] = __ldg(a.map.ex_info + e);
+    if (pairs) {
+      pinfo[e] = __ldg(a.map.pair_info + e);
+      pinfo_bhi[e] = __ldg(a.map.pair_bhi + e);
+    }
+  }
+  for (int p = tid + kSmallThreads; p < R; p += kSmallThreads) rep[p] = __ldg(a.map.rep_info + p);
+  for (int i = tid + kSmallThreads; i < N * W; i += kSmallThreads) {
+    pin[i] = __ldg(a.map.pin_mask + i);
+    hmk[i] = __ldg(a.map.host_mask + i);
+  }
+  if (tid < 32) s_load[tid] = 0;
+  if (tid == 0) s_bad = INT_MAX;
+  if (a.trace && tid == 0) a.trace[14] = (uint64_t)(clock64() - c0);
+  __syncthreads();
+  if (a.trace && tid == 0) {
+    a.trace[1] = globaltimer();
+    a.trace[15] = (uint64_t)(clock64() - c0);
+  }
+
+  // ---- pass 1: warp histogram + the activated set --------------------------
+  __shared__ int32_t s_scan[64];
+  int32_t *mycnt = cnt + warp * E;
+#pragma unroll
+  for (int i = 0; i < kSmallMaxIt; ++i) {
+    if (i >= nit) break;
+    const int sl = beg + i * 32 + lane;
+    const bool in = sl < end;
+    const int e = in ? v[i] : 0;
+    const bool valid = in && e >= 0 && e < E;
+    if (in && !valid) atomicMin(&s_bad, e);
+    const unsigned vm = __ballot_sync(kFull, valid);
+    const unsigned peers = peers_nb<NB>(vm, e, a.id_bits);
+    if (valid && lane == __ffs(peers) - 1) {
+      seen[e] = 1;  // plain byte stores: warp 0 ballots them into the activated set
+      mycnt[e] += __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (s_bad != INT_MAX) {
+    write_error_layout(a, JANUS_EUNKNOWN_EXPERT, s_bad);
+    return;
+  }
+  if (a.trace && tid == 0) a.trace[2] = globaltimer();
+
+  if (warp == 0) {
+    // ---- the activated set, pins, the sequential greedy (aebs.cpp:180-194) --
+    for (int w = 0; w < W; ++w) {
+      const unsigned b = __ballot_sync(kFull, w * 32 + lane < E && seen[w * 32 + lane]);
+      if (lane == 0) act[w] = b;
+    }
+    __syncwarp();
+    int pins = 0;
+    if (lane < N)
+      for (int w = 0; w < W; ++w) pins += __popc(act[w] & pin[lane * W + w]);
+    if (a.policy == JANUS_POLICY_AEBS && pairs) {
+      if (lane < N) s_load[lane] = pins;
+      __syncwarp();
+      greedy_pairs(
+          lane, W, N, a.map.pairs_only != 0, [&](int w) { return act[w] & multi[w]; },
+          [&](int e) { return (uint32_t)exi[e].z; }, s_load, pinfo, pinfo_bhi, plist, pb_hi,
+          elist, res, chg, s_load);
+    } else if (a.policy == JANUS_POLICY_AEBS) {
+      // 9..32 instances: lane g keeps key_g = load << 5 | g; the candidate
+      // test reads lane g's own bitmask of the multi-replica experts it hosts
+      uint32_t key = lane < N ? ((uint32_t)pins << 5) | (uint32_t)lane : 0xffffffffu;
+      for (int w = 0; w < W; ++w) {
+        unsigned mm = act[w] & multi[w];
+        const uint32_t mine = lane < N ? hmk[lane * W + w] : 0u;
+        while (mm) {
+          const int b = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const uint32_t drop = ((mine >> b) & 1u) ? 0u : 0xffffffffu;
+          const uint32_t win = __reduce_min_sync(kFull, key | drop);
+          key += (key == win) ? 32u : 0u;
+          if (lane == 0) chg[w * 32 + b] = (int)(win & 31u);
+        }
+      }
+      if (lane < N) s_load[lane] = (int)(key >> 5);
+    } else {  // schedule_random, aebs.cpp:250-262: ascending e, one lane
+      if (lane < N) s_load[lane] = pins;
+      __syncwarp();
+      if (lane == 0) {
+        uint64_t st = a.rng_state;
+        for (int w = 0; w < W; ++w)
+          for (unsigned mm = act[w] & multi[w]; mm; mm &= mm - 1) {
+            const int e = w * 32 + __ffs(mm) - 1;
+            const int4 x = exi[e];
+            const int pick = (int)next_below(st, (uint64_t)x.y);
+            // the pick-th set bit of the host mask
+            uint32_t hm = (uint32_t)x.z;
+            for (int i = 0; i < pick; ++i) hm &= hm - 1;
+            const int g = __ffs(hm) - 1;
+            chg[e] = g;
+            s_load[g] += 1;
+          }
+      }
+    }
+  } else {
+    // ---- meanwhile: per-expert totals and each warp's starting rank ---------
+    for (int e = tid - 32; e < E; e += kSmallThreads - 32) {
+      int run = 0;
+#pragma unroll
+      for (int w = 0; w < kSmallWarps; ++w) {
+        const int c = cnt[w * E + e];
+        cnt[w * E + e] = run;
+        run += c;
+      }
+      tot[e] = run;
+      const int4 x = exi[e];
+      // finish_assignment (aebs.cpp:94-108) for every expert whose instance is
+      // known now: inactive, or pinned (one replica); warp 0 finishes the
+      // multi-replica ones after its greedy
+      if (run == 0) {
+        chg[e] = -1;
+      } else if (x.y == 1) {
+        chg[e] = x.w;
+        const int2 rq = rep[x.x];
+        ridof[e] = rq.x;
+        qof[e] = rq.y;
+        qcnt[rq.y] = run;
+        tcnt[rq.y] = a.merge_tail ? max(1, run / a.tile_n) : (run + a.tile_n - 1) / a.tile_n;
+      }
+      if (run == 0 || x.y == 1) {
+        a.out.expert_instance[e] = run == 0 ? -1 : x.w;
+        if (a.out.expert_tokens) a.out.expert_tokens[e] = run;
+      }
+    }
+  }
+  if (a.trace && tid == 32) a.trace[12] = (uint64_t)(clock64() - c0);  // warp 1 done
+  __syncthreads();
+  if (a.trace && tid == 0) {
+    a.trace[4] = globaltimer();
+    a.trace[13] = (uint64_t)(clock64() - c0);
+  }
+
+  // ---- finish the multi-replica experts the greedy placed (the others were
+  // finished during the greedy), then the group offsets ----------------------
+  for (int e = tid; e < E; e += kSmallThreads)
+    if (((act[e >> 5] & multi[e >> 5]) >> (e & 31)) & 1u)
+      finish_multi(a, e, chg[e], exi[e], rep, tot, chg, ridof, qof, qcnt, tcnt);
+  __syncthreads();
+  block_exscan2<kSmallThreads>(qcnt, tcnt, R + 1, s_scan);
+  if (a.out.group_off)
+    for (int q = tid; q <= R; q += kSmallThreads) a.out.group_off[q] = qcnt[q];
+  if (a.tile_off)
+    for (int q = tid; q <= R; q += kSmallThreads) a.tile_off[q] = tcnt[q];
+  if (a.shared_off && tid == 0) {
+    const int rows = a.shared_rows;
+    a.shared_off[0] = 0;
+    a.shared_off[1] = rows;
+    a.shared_off[2] = 0;
+    a.shared_off[3] = rows > 0 ? (rows + a.shared_tile_n - 1) / a.shared_tile_n : 0;
+  }
+  if (tid < N) {  // an instance's groups are contiguous in replica order
+    a.out.load[tid] = s_load[tid];
+    a.out.routed_tokens[tid] = (int64_t)(qcnt[qb[tid + 1]] - qcnt[qb[tid]]);
+  }
+  if (a.trace && tid == 0) a.trace[5] = globaltimer();
+
+  // ---- pass 2: remap slots and lay out rows --------------------------------
+#pragma unroll
+  for (int i = 0; i < kSmallMaxIt; ++i) {
+    if (i >= nit) break;
+    const int sl = beg + i * 32 + lane;
+    const bool in = sl < end;
+    const int e = in ? v[i] : 0;
+    const unsigned vm = __ballot_sync(kFull, in);
+    const unsigned peers = peers_nb<NB>(vm, e, a.id_bits);
+    if (in) {
+      const int rank = __popc(peers & lanemask_lt());
+      const int cbase = mycnt[e];
+      const int row = qcnt[qof[e]] + cbase + rank;
+      __syncwarp(vm);
+      if (lane == __ffs(peers) - 1) mycnt[e] = cbase + __popc(peers);
+      a.out.instance[sl] = chg[e];
+      a.out.replica[sl] = ridof[e];
+      if (a.out.slot_row) a.out.slot_row[sl] = row;
+      if (a.out.row_slot) a.out.row_slot[row] = sl;
+    }
+    __syncwarp();
+  }
+  if (tid == 0) {
+    a.out.status[0] = JANUS_OK;
+    a.out.status[1] = 0;
+  }
+  if (a.trace) {
+    __syncthreads();
+    if (tid == 0) {
+      a.trace[3] = a.trace[2];  // no separate pin phase
+      a.trace[6] = globaltimer();
+      a.trace[7] = (uint64_t)(clock64() - c0);  // SM cycles over the kernel (clock rate)
+    }
+  }
+}
+
+size_t small_smem_bytes(int E, int N, int R) {
+  return small_absent_off(E, N, R) + (size_t)16 * (2 * E + 4) + (size_t)4 * (4 * E + 24) +
+         (size_t)E;
+}
+
 template <int MAXIT>
 cudaError_t launch_variant(const SchedArgs &a, size_t smem, int csize, cudaStream_t stream) {
   // The opt-in smem limit is per device and per function; raise it when a
@@ -515,8 +1050,12 @@ cudaError_t launch_variant(const SchedArgs &a, size_t smem, int csize, cudaStrea
 }  // namespace
 
 size_t schedule_smem_bytes(int E, int N, int R) {
-  return (size_t)N * 4 + (size_t)32 * E * 4 + (size_t)6 * E * 4 + (size_t)N * 4 +
-         (size_t)2 * (R + 1) * 4 + (size_t)(E + 1) * 4 + (size_t)3 * R * 4 + (size_t)E * 4;
+  const size_t base = (size_t)N * 4 + (size_t)32 * E * 4 + (size_t)6 * E * 4 + (size_t)N * 4 +
+                      (size_t)2 * (R + 1) * 4 + (size_t)(E + 1) * 4 + (size_t)3 * R * 4 +
+                      (size_t)E * 4;
+  if (N > 8) return base;
+  const size_t E4 = (E + 3) & ~3;  // + the pairs greedy's records and list
+  return base + 16 + (size_t)16 * (2 * E + 4) + (size_t)4 * (4 * E4 + 8);
 }
 
 int schedule_cluster_size(int S) {
@@ -531,6 +1070,36 @@ int schedule_cluster_size(int S) {
 }
 
 cudaError_t launch_schedule(const SchedArgs &a, cudaStream_t stream) {
+  // JANUS_SCHED_CLUSTER=1 forces the cluster kernel at every size (A/B runs)
+  static const bool force_cluster = std::getenv("JANUS_SCHED_CLUSTER") != nullptr;
+  if (a.S <= kSmallMaxSlots && a.map.N <= 32 && a.map.R <= kSmallMaxReplicas && a.map.host_mask &&
+      !force_cluster) {
+    const size_t smem = small_smem_bytes(a.map.E, a.map.N, a.map.R);
+    if (smem <= 200 * 1024) {
+      static int configured_dev = -1;
+      static size_t configured_smem = 0;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (configured_dev != dev || smem > configured_smem) {
+        const size_t want = smem > 48 * 1024 ? smem : 48 * 1024;
+        for (auto k : {aebs_small_kernel<0>, aebs_small_kernel<6>, aebs_small_kernel<7>,
+                       aebs_small_kernel<8>}) {
+          cudaError_t err =
+              cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+          if (err != cudaSuccess) return err;
+        }
+        configured_dev = dev;
+        configured_smem = want;
+      }
+      // the id width the BASELINE configs use (E = 64 / 128 / 256) unrolled
+      auto k = a.id_bits == 6   ? aebs_small_kernel<6>
+               : a.id_bits == 7 ? aebs_small_kernel<7>
+               : a.id_bits == 8 ? aebs_small_kernel<8>
+                                : aebs_small_kernel<0>;
+      k<<<1, kSmallThreads, smem, stream>>>(a);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = schedule_smem_bytes(a.map.E, a.map.N, a.map.R);
   const int csize = schedule_cluster_size(a.S);
   const int windows = (a.S + 31) / 32;

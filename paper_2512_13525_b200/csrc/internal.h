@@ -17,8 +17,30 @@ constexpr int kSchedThreads = 1024;  // one CTA, 32 warps
 // Map-derived tables on the device (uploaded once per janus_set_replica_map).
 struct DevMap {
   int E = 0, N = 0, C = 0, R = 0;
+  void *blob = nullptr;  // the one allocation every table below points into
   int32_t *off = nullptr, *hosts = nullptr, *rid = nullptr, *qidx = nullptr;
   uint32_t *hmask = nullptr;  // per-expert host bitmask (N <= 32 only)
+  // compact tables of the single-CTA decode scheduler (N <= 32): per expert
+  // {off, replicas, host bitmask, first host}; per replica {rid, qidx}; the
+  // multi-replica experts and, per instance, its single-replica experts as
+  // bitmasks of ceil(E/32) words ([E/32] and [N][E/32])
+  int4 *ex_info = nullptr;
+  int2 *rep_info = nullptr;
+  uint32_t *multi_mask = nullptr, *pin_mask = nullptr;
+  // host_mask [N][E/32]: the multi-replica experts hosted on instance g (the
+  // greedy's candidate test without a shuffle); qbase [N+1]: first replica of
+  // instance g in replica order (routed_tokens from the scanned group offsets)
+  uint32_t *host_mask = nullptr;
+  int32_t *qbase = nullptr;
+  // pair_info [E] + pair_bhi [E] (N <= 8 and C <= 255: loads fit a byte), the
+  // one-lane greedy's record per multi-replica expert.  Two hosts a < b:
+  // {a << 12 | b << 28 (PRMT selectors: load[a] / load[b] as the top byte
+  // over identical low bytes), +1 at a in the lo / hi load word, +1 at b in
+  // the lo word}, pair_bhi = +1 at b in the hi word.  Three or more:
+  // {~0, host bitmask, 0, 0}.
+  uint4 *pair_info = nullptr;
+  uint32_t *pair_bhi = nullptr;
+  int pairs_only = 0;  // every multi-replica expert has exactly two hosts
 };
 
 struct SchedArgs {

@@ -8,7 +8,8 @@ Same names, argument meaning and error behaviour as the reference C++ library
   :class:`ValidationError` (include/moesim/types.hpp:20-22).
 * :func:`schedule`, :func:`schedule_random` (aebs.hpp:63-71) — run on the GPU by
   the fused sm_100a scheduler kernel; there is no CPU path.
-* :class:`RoutingPattern`, :func:`gen_batch` (include/moesim/workload.hpp:14-32).
+* synthetic routing (RoutingPattern / gen_batch, workload.hpp:14-32) is not
+  part of the product: tests and the bench use oracle/routing.py.
 * text formats :func:`load_batch`, :func:`load_replica_map`,
   :func:`dump_assignment` (src/aebs.cpp:338-479); ``load_replica_map`` also reads
   the explicit-id extension ``expert: instance:replica_id ...`` used by the
@@ -18,7 +19,6 @@ Same names, argument meaning and error behaviour as the reference C++ library
 from __future__ import annotations
 
 import ctypes as C
-import math
 import os
 from dataclasses import dataclass, field
 
@@ -292,76 +292,6 @@ def schedule_random(batch: ActivationBatch, rmap: ReplicaMap, seed: int) -> Assi
 
 
 # --------------------------------------------------------------- workload --
-
-@dataclass
-class RoutingPattern:
-    """workload.hpp:14-28 (pmf normalised in order, inclusive cdf, back() == 1)."""
-
-    pmf: np.ndarray
-    cdf: np.ndarray
-
-    @staticmethod
-    def from_pmf(weights) -> "RoutingPattern":
-        w = [float(x) for x in weights]
-        if not w:
-            raise ValidationError("routing: empty pmf")
-        s = 0.0
-        for x in w:
-            if not x >= 0:
-                raise ValidationError("routing: pmf weights must be >= 0")
-            s += x
-        if s <= 0:
-            raise ValidationError("routing: pmf sums to zero")
-        pmf = np.array([x / s for x in w], np.float64)
-        cdf = np.zeros_like(pmf)
-        acc = 0.0
-        for i, p in enumerate(pmf):
-            acc += float(p)
-            cdf[i] = acc
-        cdf[-1] = 1.0
-        return RoutingPattern(pmf, cdf)
-
-    @staticmethod
-    def uniform(num_experts: int) -> "RoutingPattern":
-        if num_experts < 1:
-            raise ValidationError("routing: num_experts must be >= 1")
-        return RoutingPattern.from_pmf([1.0] * num_experts)
-
-    @staticmethod
-    def gaussian(num_experts: int, sigma: float) -> "RoutingPattern":
-        if num_experts < 1:
-            raise ValidationError("routing: num_experts must be >= 1")
-        if not sigma > 0:
-            raise ValidationError("routing: sigma must be > 0")
-        center = num_experts / 2.0
-        denom = 2.0 * (sigma * num_experts) * (sigma * num_experts)
-        return RoutingPattern.from_pmf(
-            [math.exp(-((e - center) ** 2) / denom) for e in range(num_experts)])
-
-    @staticmethod
-    def zipf(num_experts: int, s: float) -> "RoutingPattern":
-        """Zipf via from_pmf(1/(e+1)^s) (the reference has no zipf kind)."""
-        return RoutingPattern.from_pmf([1.0 / (e + 1) ** s for e in range(num_experts)])
-
-    def num_experts(self) -> int:
-        return len(self.pmf)
-
-
-def gen_batch(pattern: RoutingPattern, num_tokens: int, top_k: int, seed: int,
-              step: int) -> ActivationBatch:
-    """workload.hpp:29-32 (bit-exact; host-side input generation)."""
-    E = pattern.num_experts()
-    if num_tokens < 0:
-        raise ValidationError("gen_batch: negative num_tokens")
-    if top_k < 1 or top_k > E:
-        raise ValidationError("gen_batch: top_k out of range")
-    out = np.zeros(num_tokens * top_k, np.int32)
-    cdf = np.ascontiguousarray(pattern.cdf, np.float64)
-    st = lib.janus_gen_batch(_ptr(cdf), E, num_tokens, top_k, seed, step, _ptr(out))
-    if st != OK:
-        raise ValidationError("gen_batch: invalid arguments")
-    return ActivationBatch(num_tokens, top_k, out)
-
 
 def derive_seed(root: int, label: str, extra: int = 0) -> int:
     return int(lib.janus_derive_seed(root, label.encode(), extra))

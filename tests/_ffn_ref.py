@@ -50,3 +50,49 @@ def assert_close(dev, ref, rtol, atol, what=""):
     assert not bad.any(), (f"{what}: {bad.sum()} / {bad.size} outside tolerance; max err "
                            f"{err.max():.4g}, rms(ref) {rms:.4g}")
     return float(err.max() / rms)
+
+
+def bf16_round(a):
+    """fp32 -> nearest-even bf16 -> fp32 (numpy)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+def moe_reference_device_exact(oracle, x_u16, ex, w, weights_of, nthreads=8):
+    """The device's rounding points, restated: h rounded to bf16 (between the
+    GEMMs), y rounded to bf16 (the down GEMM's output rows), the combine
+    out[t] = fma(w_j, y_j, acc) over j ascending in fp32 (K5, ffn.cu), out
+    rounded to bf16.  Returns (out as the fp32 values of bf16 numbers,
+    sum_j |w_j y_j| per element)."""
+    T, k = ex.shape
+    d_h = x_u16.shape[1]
+    y = np.zeros((T, k, d_h), np.float32)
+    by_e = {}
+    for t in range(T):
+        for j in range(k):
+            by_e.setdefault(int(ex[t, j]), []).append((t, j))
+    for e, lst in sorted(by_e.items()):
+        wg, wu, wd = weights_of(e)
+        rows = np.stack([x_u16[t] for t, _ in lst])
+        ye = bf16_round(oracle.expert_swiglu(rows, wg, wu, wd, round_h=True, nthreads=nthreads))
+        for r, (t, j) in enumerate(lst):
+            y[t, j] = ye[r]
+    acc = np.zeros((T, d_h), np.float32)
+    mag = np.zeros((T, d_h), np.float64)
+    for j in range(k):  # fma: the f32 product is exact in f64; one rounding to f32
+        p = w[:, j:j + 1].astype(np.float64) * y[:, j].astype(np.float64)
+        acc = (acc.astype(np.float64) + p).astype(np.float32)
+        mag += np.abs(p)
+    return bf16_round(acc), mag
+
+
+def ulp_stats(dev, ref, mag):
+    """dev, ref: fp32 values of bf16 numbers; mag = sum_j |w_j y_j| (the
+    combine's magnitude).  (fraction bit-identical, max |dev - ref| in bf16
+    ulps of mag) — a 1-ulp flip of some y_j's rounding moves out by at most
+    w_j ulp(y_j) <= ulp(mag), whatever cancellation the sum has."""
+    same = float(np.mean(dev.view(np.uint32) == ref.view(np.uint32)))
+    e = np.floor(np.log2(np.maximum(np.abs(mag), 1e-30)))
+    ulp = np.exp2(e - 7)
+    return same, float(np.max(np.abs(dev - ref) / ulp))

@@ -46,17 +46,6 @@ def test_library_is_sm100a(J):
         assert mnem in sass, mnem
 
 
-def test_gen_batch_matches_oracle(J, oracle):
-    for pat, cdf in ((J.RoutingPattern.gaussian(64, 0.15), oracle.pattern("gaussian", 64)[1]),
-                     (J.RoutingPattern.zipf(128, 1.0),
-                      oracle.pattern("pmf", 128, weights=[1 / (e + 1) for e in range(128)])[1]),
-                     (J.RoutingPattern.uniform(200), oracle.pattern("uniform", 200)[1])):
-        assert np.array_equal(pat.cdf, cdf)
-        for T in (0, 1, 255, 256, 4096):
-            b = J.gen_batch(pat, T, 8, 0x5EED, T)
-            assert np.array_equal(b.experts, oracle.gen_batch(cdf, T, 8, 0x5EED, T))
-
-
 def test_derive_seed(J, oracle):
     for r, l, x in ((0, "a", 0), (42, "sched/random", 0), (7, "workload/step", 99)):
         assert J.derive_seed(r, l, x) == oracle.derive_seed(r, l, x)

@@ -13,6 +13,7 @@ import pytest
 
 from test_gpu_moe import check_close, make_layer, oracle_layer_out, run, u16  # noqa: F401
 from oracle import bf16_to_f32
+from routing import RoutingPattern, gen_batch
 
 pytestmark = pytest.mark.gpu
 CASES = int(os.environ.get("JANUS_FUZZ_CASES", "64"))
@@ -52,22 +53,23 @@ def test_layer_fuzz(J, oracle, case):
     rm = random_map(J, rng, E, N)
     instance = -1 if N == 1 or rng.random() < 0.5 else int(rng.integers(0, N))
     shared = bool(rng.random() < 0.25) and instance <= 0
-    pat = (J.RoutingPattern.zipf(E, float(rng.choice([0.0, 1.0, 1.5]))) if rng.random() < 0.7
-           else J.RoutingPattern.gaussian(E, 0.2))
-    b = J.gen_batch(pat, T, k, int(rng.integers(1 << 30)), case)
+    pat = (RoutingPattern.zipf(E, float(rng.choice([0.0, 1.0, 1.5]))) if rng.random() < 0.7
+           else RoutingPattern.gaussian(E, 0.2))
+    b = gen_batch(pat, T, k, int(rng.integers(1 << 30)), case)
     layer = make_layer(J, rm, d_h, d_e, max(T, 1), k, seed=case + 1, instance=instance)
     if shared:
         wg, wu, wd = expert_weights(E + 1, d_h, d_e, case + 3, "cuda")
         layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
     x, ex, gw, out = run(J, layer, b.experts, T, seed=case + 7)
     tokens = np.unique(np.concatenate([[0, T - 1], rng.integers(0, T, 24)]))
-    ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens)
-    if shared:
-        ref += oracle.expert_swiglu(u16(x)[tokens], u16(wg), u16(wu), u16(wd), round_h=True,
-                                    nthreads=8)
     what = (f"case {case}: E={E} k={k} d_h={d_h} d_e={d_e} T={T} N={N} instance={instance} "
             f"shared={shared}")
-    check_close(bf16_to_f32(u16(out))[tokens], ref, what)
+    for round_h in (True, False):  # h rounded like the device, and the pure fp32 layer
+        ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens, round_h=round_h)
+        if shared:
+            ref += oracle.expert_swiglu(u16(x)[tokens], u16(wg), u16(wu), u16(wd),
+                                        round_h=round_h, nthreads=8)
+        check_close(bf16_to_f32(u16(out))[tokens], ref, what + f" round_h={round_h}")
 
 
 @pytest.mark.parametrize("case", range(CASES))
@@ -82,8 +84,8 @@ def test_scheduler_fuzz(J, oracle, case):
     k = int(rng.choice([k_ for k_ in (1, 2, 4, 8) if k_ <= E]))
     T = int(rng.choice([0, 1, int(rng.integers(2, 300)), int(rng.integers(300, 6000))]))
     rm = random_map(J, rng, E, N)
-    pat = J.RoutingPattern.zipf(E, float(rng.choice([0.0, 1.0, 1.2])))
-    b = J.gen_batch(pat, T, k, int(rng.integers(1 << 30)), case)
+    pat = RoutingPattern.zipf(E, float(rng.choice([0.0, 1.0, 1.2])))
+    b = gen_batch(pat, T, k, int(rng.integers(1 << 30)), case)
     m = CSRMap(rm.num_experts, rm.num_instances, rm.slots_per_instance, *rm.csr())
     sched = J.Scheduler(rm)
     try:

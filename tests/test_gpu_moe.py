@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 from oracle import CSRMap, bf16_to_f32
+from routing import RoutingPattern, gen_batch
 
 pytestmark = pytest.mark.gpu
 RTOL = 2.0 ** -6
@@ -30,9 +31,10 @@ def u16(t):
     return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-def oracle_layer_out(oracle, layer, x, experts, gw, tokens=None):
+def oracle_layer_out(oracle, layer, x, experts, gw, tokens=None, round_h=True):
     """fp32 reference of out[t] for the given tokens (all by default).  For a
-    single-instance layer only the slots AEBS assigns to that instance count."""
+    single-instance layer only the slots AEBS assigns to that instance count.
+    round_h: h rounded to bf16 where the device rounds it (False: pure fp32)."""
     T = x.shape[0]
     k = layer.k
     tokens = np.arange(T) if tokens is None else np.asarray(tokens)
@@ -61,7 +63,7 @@ def oracle_layer_out(oracle, layer, x, experts, gw, tokens=None):
         w13 = u16(layer.w13[q])
         wd = u16(layer.w2[q])
         rows = np.stack([xu[t] for _, t, _ in lst])
-        y = oracle.expert_swiglu(rows, w13[:d_e], w13[d_e:], wd, round_h=True, nthreads=8)
+        y = oracle.expert_swiglu(rows, w13[:d_e], w13[d_e:], wd, round_h=round_h, nthreads=8)
         for r, (i, t, j) in enumerate(lst):
             out[i] += w[t, j] * y[r]
     return out
@@ -99,7 +101,7 @@ def run(J, layer, experts_np, T, seed=3):
 def test_small_layer_all_tokens(J, oracle, T):
     rm = J.ReplicaMap.from_hosts(1, 8, [[0]] * 8)
     layer = make_layer(J, rm, 256, 128, 512, 2)
-    b = J.gen_batch(J.RoutingPattern.uniform(8), T, 2, 11, T)
+    b = gen_batch(RoutingPattern.uniform(8), T, 2, 11, T)
     x, ex, gw, out = run(J, layer, b.experts, T)
     ref = oracle_layer_out(oracle, layer, x, ex, gw)
     check_close(bf16_to_f32(u16(out)), ref, f"T={T}")
@@ -109,7 +111,7 @@ def test_ragged_groups_multiple_n_tiles(J, oracle):
     # 4 experts, 1000 tokens, k=2 -> groups of ~500 rows: 4+ n-tiles each, ragged tails
     rm = J.ReplicaMap.from_hosts(1, 4, [[0]] * 4)
     layer = make_layer(J, rm, 512, 256, 1000, 2)
-    b = J.gen_batch(J.RoutingPattern.zipf(4, 1.0), 1000, 2, 5, 0)
+    b = gen_batch(RoutingPattern.zipf(4, 1.0), 1000, 2, 5, 0)
     x, ex, gw, out = run(J, layer, b.experts, 1000)
     ref = oracle_layer_out(oracle, layer, x, ex, gw)
     check_close(bf16_to_f32(u16(out)), ref, "ragged")
@@ -121,7 +123,7 @@ def test_replicated_map_all_instances_local(J, oracle):
     hosts = [[0, 1], [1, 2], [0, 2], [0], [1], [2], [0, 1, 2], [2]] * 2
     rm = J.ReplicaMap.from_hosts(3, 12, hosts)
     layer = make_layer(J, rm, 256, 128, 256, 4)
-    b = J.gen_batch(J.RoutingPattern.gaussian(16, 0.2), 200, 4, 9, 1)
+    b = gen_batch(RoutingPattern.gaussian(16, 0.2), 200, 4, 9, 1)
     x, ex, gw, out = run(J, layer, b.experts, 200)
     ref = oracle_layer_out(oracle, layer, x, ex, gw)
     check_close(bf16_to_f32(u16(out)), ref, "replicated")
@@ -131,7 +133,7 @@ def test_per_instance_partials_sum_to_full(J, oracle):
     import torch
     hosts = [[0, 1], [1, 2], [0, 2], [0], [1], [2], [0, 1, 2], [2]] * 2
     rm = J.ReplicaMap.from_hosts(3, 12, hosts)
-    b = J.gen_batch(J.RoutingPattern.gaussian(16, 0.2), 200, 4, 9, 1)
+    b = gen_batch(RoutingPattern.gaussian(16, 0.2), 200, 4, 9, 1)
     full = make_layer(J, rm, 256, 128, 256, 4)
     x, ex, gw, out_full = run(J, full, b.experts, 200)
     acc = torch.zeros(200, 256, dtype=torch.float32, device="cuda")
@@ -149,7 +151,7 @@ def test_qwen3_30b_shape_sampled_tokens(J, oracle):
     # c2: Qwen3-30B-A3B expert shape, the committed c2 map, Zipf-1.0 routing
     rm = J.config_map("c2")
     layer = make_layer(J, rm, 2048, 768, 256, 8)
-    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), 256, 8, 0x30, 256)
+    b = gen_batch(RoutingPattern.zipf(128, 1.0), 256, 8, 0x30, 256)
     x, ex, gw, out = run(J, layer, b.experts, 256)
     tokens = np.random.default_rng(0).choice(256, 48, replace=False)
     ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens)
@@ -163,7 +165,7 @@ def test_qwen3_30b_bench_size_sampled_tokens(J, oracle, T):
     sampled tokens vs the fp32 oracle, the first and last tokens included."""
     rm = J.config_map("c2")
     layer = make_layer(J, rm, 2048, 768, T, 8)
-    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, 8, 0x30, T * 1000)
+    b = gen_batch(RoutingPattern.zipf(128, 1.0), T, 8, 0x30, T * 1000)
     x, ex, gw, out = run(J, layer, b.experts, T)
     tokens = np.concatenate([[0, T - 1], np.random.default_rng(T).choice(
         np.arange(1, T - 1), 46, replace=False)])
@@ -177,7 +179,7 @@ def test_layer_assignment_bit_exact_and_host_e2e(J, oracle):
     m = load_map_csr("c3")
     rm = J.config_map("c3")
     layer = make_layer(J, rm, 256, 128, 512, 8)
-    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), 512, 8, 0x235, 512)
+    b = gen_batch(RoutingPattern.zipf(128, 1.0), 512, 8, 0x235, 512)
     S, R = 512 * 8, int(m.off[-1])
     d = lambda n, dt=torch.int32: torch.zeros(n, dtype=dt, device="cuda")
     asg = dict(instance=d(S), replica=d(S), expert_instance=d(m.E), load=d(m.N),
@@ -234,7 +236,7 @@ def test_pipelined_host_api_matches_device_path(J):
     from paper_2512_13525_b200.moe import make_inputs
     calls = []
     for i in range(5):
-        b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, k, 0x30, i)
+        b = gen_batch(RoutingPattern.zipf(128, 1.0), T, k, 0x30, i)
         x, gw = make_inputs(T, k, 2048, i, "cuda")
         ex = torch.from_numpy(b.experts).cuda()
         ref = layer.forward(x, ex, gw).cpu()
@@ -265,7 +267,7 @@ def test_shared_expert(J, oracle, T):
     layer = make_layer(J, rm, 256, 128, 300, 4)
     wg, wu, wd = expert_weights(999, 256, 128, 7, "cuda")
     layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
-    b = J.gen_batch(J.RoutingPattern.zipf(16, 1.0), T, 4, 3, T)
+    b = gen_batch(RoutingPattern.zipf(16, 1.0), T, 4, 3, T)
     x, ex, gw, out = run(J, layer, b.experts, T)
     ref = oracle_layer_out(oracle, layer, x, ex, gw)
     ref += oracle.expert_swiglu(u16(x), u16(wg), u16(wu), u16(wd), round_h=True, nthreads=8)
@@ -287,7 +289,7 @@ def test_deepseek_v3_shape_with_shared_expert_sampled_tokens(J, oracle):
     layer = make_layer(J, rm, d_h, d_e, T, k)
     wg, wu, wd = expert_weights(256, d_h, d_e, 7, "cuda")
     layer.set_shared(torch.cat([wg, wu]).contiguous(), wd.contiguous())
-    b = J.gen_batch(J.RoutingPattern.zipf(E, 1.0), T, k, 0xD5, T)
+    b = gen_batch(RoutingPattern.zipf(E, 1.0), T, k, 0xD5, T)
     x, ex, gw, out = run(J, layer, b.experts, T)
     tokens = np.random.default_rng(1).choice(T, 12, replace=False)
     ref = oracle_layer_out(oracle, layer, x, ex, gw, tokens)
@@ -303,14 +305,14 @@ def test_replica_map_reconfiguration(J, oracle):
     from paper_2512_13525_b200.moe import build_weight_store
     small = J.ReplicaMap.from_hosts(1, 8, [[0]] * 8)
     layer = make_layer(J, small, 256, 128, 200, 4)
-    b = J.gen_batch(J.RoutingPattern.uniform(8), 150, 4, 1, 0)
+    b = gen_batch(RoutingPattern.uniform(8), 150, 4, 1, 0)
     x, ex, gw, out = run(J, layer, b.experts, 150)
     check_close(bf16_to_f32(u16(out)), oracle_layer_out(oracle, layer, x, ex, gw), "before")
     hosts = [sorted({e % 3, (e * 7) % 3}) for e in range(48)]
     big = J.ReplicaMap.from_hosts(3, 48, hosts)
     layer.set_map(big)
     layer.set_weights(*build_weight_store(layer, seed=2))
-    b = J.gen_batch(J.RoutingPattern.zipf(48, 1.0), 200, 4, 2, 0)
+    b = gen_batch(RoutingPattern.zipf(48, 1.0), 200, 4, 2, 0)
     x, ex, gw, out = run(J, layer, b.experts, 200)
     check_close(bf16_to_f32(u16(out)), oracle_layer_out(oracle, layer, x, ex, gw), "after")
 
@@ -324,7 +326,7 @@ def test_box_map_full_step(J, oracle, M):
     instance's partial layer output is within tolerance on a token sample."""
     rm = J.config_map(f"c2_m{M}")
     T, k = 4096 * M, 8
-    b = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, k, 0x30, T * 1000)
+    b = gen_batch(RoutingPattern.zipf(128, 1.0), T, k, 0x30, T * 1000)
     layer = make_layer(J, rm, 2048, 768, T, k, instance=M - 1)
     off, hosts, rid = layer.sched._csr
     m = CSRMap(rm.num_experts, rm.num_instances, rm.slots_per_instance, off, hosts, rid)
@@ -336,3 +338,68 @@ def test_box_map_full_step(J, oracle, M):
     tokens = np.arange(0, T, T // 48)
     refo = oracle_layer_out(oracle, layer, x, ex, gw, tokens=tokens)
     check_close(bf16_to_f32(u16(out))[tokens], refo, f"c2_m{M} instance {M - 1}")
+
+
+# ---- parity against three references ----------------------
+PARITY_CASES = {
+    # name: (E, d_h, d_e, k, T, routing, sampled tokens or None)
+    "small_e8": (8, 256, 128, 2, 300, ("uniform", 11), None),
+    "c2_t256": (128, 2048, 768, 8, 256, ("zipf", 0x30), 64),
+    "c2_t4096": (128, 2048, 768, 8, 4096, ("zipf", 0x30), 64),
+    "c3_shape_e16": (16, 4096, 1536, 8, 512, ("zipf", 0x235), 48),
+}
+
+
+@pytest.mark.parametrize("name", sorted(PARITY_CASES))
+def test_layer_parity_vs_fp32_and_device_exact(J, oracle, name):
+    """Each layer output element against
+      (1) the pure fp32 layer (h, y, out fp32):   |d - r| <= 2^-6 |r| + 2^-6 rms(r);
+      (2) h rounded like the device:              same bound;
+      (3) the device-exact restatement (h, y rounded to bf16, fma combine in
+          j order, out rounded to bf16): at most 2 bf16 ulps of the combine's
+          magnitude sum_j |w_j y_j|, and >= 85 % of the elements bit-identical —
+          the remaining differences come from fp32 accumulation order inside
+          the tensor-core GEMMs flipping a bf16 rounding of h or y.
+    The measured figures are appended to gpurun_out/ffn_parity_stats.jsonl
+    (DESIGN.md §2 records them)."""
+    import json
+    import os
+    from _ffn_ref import (assert_close, err_stats, moe_reference, moe_reference_device_exact,
+                          ulp_stats)
+    E, d_h, d_e, k, T, (kind, seed), ns = PARITY_CASES[name]
+    rm = J.config_map("c2") if E == 128 else J.ReplicaMap.from_hosts(1, E, [[0]] * E)
+    layer = make_layer(J, rm, d_h, d_e, T, k)
+    pat = RoutingPattern.uniform(E) if kind == "uniform" else RoutingPattern.zipf(E, 1.0)
+    b = gen_batch(pat, T, k, seed, T)
+    x, ex, gw, out = run(J, layer, b.experts, T)
+    tokens = (np.arange(T) if ns is None else
+              np.unique(np.concatenate([[0, T - 1], np.random.default_rng(T).choice(T, ns)])))
+    q_of = {}
+    for q, e in enumerate(layer.local_experts()):
+        q_of.setdefault(int(e), q)
+    cache = {}
+
+    def weights_of(e):
+        if e not in cache:
+            w13 = u16(layer.w13[q_of[e]])
+            cache[e] = (w13[:d_e], w13[d_e:], u16(layer.w2[q_of[e]]))
+        return cache[e]
+    xs = u16(x)[tokens]
+    exn = ex.cpu().numpy().reshape(T, k)[tokens]
+    wn = gw.cpu().numpy().reshape(T, k)[tokens]
+    dev = bf16_to_f32(u16(out))[tokens]
+    ref_f = moe_reference(oracle, xs, exn, wn, weights_of, round_h=False)
+    ref_h = moe_reference(oracle, xs, exn, wn, weights_of, round_h=True)
+    ref_x, mag = moe_reference_device_exact(oracle, xs, exn, wn, weights_of)
+    assert_close(dev, ref_f, 2.0 ** -6, 2.0 ** -6, f"{name} vs pure fp32")
+    assert_close(dev, ref_h, 2.0 ** -6, 2.0 ** -6, f"{name} vs round_h")
+    same, max_ulp = ulp_stats(dev, ref_x, mag)
+    stats = {"case": name, "T": T, "tokens_checked": int(len(tokens)),
+             "max_err_over_rms_fp32": err_stats(dev, ref_f)[0],
+             "max_err_over_rms_round_h": err_stats(dev, ref_h)[0],
+             "device_exact_bit_identical": same, "device_exact_max_ulp": max_ulp}
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(root, "gpurun_out", "ffn_parity_stats.jsonl"), "a") as f:
+        f.write(json.dumps(stats) + "\n")
+    assert max_ulp <= 2.0 and same >= 0.85, stats

@@ -6,18 +6,19 @@ import torch
 
 import paper_2512_13525_b200 as J
 from paper_2512_13525_b200.moe import ActivationStats
+from routing import RoutingPattern, gen_batch
 
 pytestmark = pytest.mark.gpu
 
 
 def _steps(E, k, n, seed, T_choices=(0, 1, 3, 17, 64, 300)):
     rng = np.random.default_rng(seed)
-    pats = [J.RoutingPattern.uniform(E), J.RoutingPattern.zipf(E, 1.2),
-            J.RoutingPattern.gaussian(E, 0.1)]
+    pats = [RoutingPattern.uniform(E), RoutingPattern.zipf(E, 1.2),
+            RoutingPattern.gaussian(E, 0.1)]
     out = []
     for i in range(n):
         T = int(rng.choice(T_choices))
-        out.append(J.gen_batch(pats[i % 3], T, k, seed, i).experts)
+        out.append(gen_batch(pats[i % 3], T, k, seed, i).experts)
     return out
 
 

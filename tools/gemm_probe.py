@@ -18,6 +18,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+from routing import RoutingPattern, gen_batch  # noqa: E402
 
 import paper_2512_13525_b200 as J  # noqa: E402
 from paper_2512_13525_b200._lib import lib  # noqa: E402
@@ -72,10 +74,10 @@ def main():
             ex = ((np.arange(T)[:, None] * 8 + np.arange(8)[None, :]) % 128).astype(np.int32).ravel()
         elif name == "uni128":
             rmap = J.ReplicaMap.from_hosts(1, 128, [[0]] * 128)
-            ex = J.gen_batch(J.RoutingPattern.uniform(128), T, K, 0x77, 0).experts
+            ex = gen_batch(RoutingPattern.uniform(128), T, K, 0x77, 0).experts
         else:
             rmap = J.config_map("c2")
-            ex = J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, K, 0x30, T * 1000).experts
+            ex = gen_batch(RoutingPattern.zipf(128, 1.0), T, K, 0x30, T * 1000).experts
         probe(name, rmap, ex, T)
 
 

@@ -11,6 +11,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+from routing import RoutingPattern, gen_batch  # noqa: E402
 import paper_2512_13525_b200 as J  # noqa: E402
 from paper_2512_13525_b200.moe import MoELayer, build_weight_store, make_inputs  # noqa: E402
 
@@ -26,7 +28,7 @@ dev = torch.device("cuda", 0)
 rmap = J.config_map("c2" if a.moe == 1 else f"c2_m{a.moe}")
 layer = MoELayer(rmap, 2048, 768, T, 8, instance=a.instance, device=0)
 layer.set_weights(*build_weight_store(layer, seed=1))
-ex = torch.from_numpy(J.gen_batch(J.RoutingPattern.zipf(128, 1.0), T, 8, 0x30, T * 1000).experts).to(dev)
+ex = torch.from_numpy(gen_batch(RoutingPattern.zipf(128, 1.0), T, 8, 0x30, T * 1000).experts).to(dev)
 x, gw = make_inputs(T, 8, 2048, 3, dev)
 out = torch.empty_like(x)
 if a.gate:
