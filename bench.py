@@ -592,7 +592,7 @@ def run_box(args):
             from paper_2512_13525_b200.moe import router_weights
             layer.set_router(router_weights(E, D_H, 13, dev))
     box = JanusBox(plan, rank, T, D_H, K_TOP, layer=layer, device=local,
-                   transport=args.transport, rmap=shape_map(J, M)[0])
+                   transport=args.transport, rmap=shape_map(J, M)[0], combine=args.combine)
     batches = [torch.from_numpy(b).to(dev) for b in gen_batches(T)]
     x, gw = make_inputs(T, K_TOP, D_H, 3, dev)
     first, cnt = plan.shard(T, rank) if att else (0, 0)
@@ -605,10 +605,11 @@ def run_box(args):
     out = torch.empty(max(cnt, 1), D_H, dtype=torch.bfloat16, device=dev)
     s = torch.cuda.current_stream(dev)
     stream = s.cuda_stream
-    # a colocated rank runs its MoE role on a second stream (NVLS transport:
-    # the two roles share no device state), so its combine of step i — which
-    # waits for every rank's MoE step i — does not hold back its MoE step i+1
-    s_moe = torch.cuda.Stream(dev) if (plan.colocated and box.transport == "nvls") else s
+    # a colocated rank runs its MoE role on a second stream (the two roles
+    # share no device state; every kernel kind has its own completion counter),
+    # so its combine of step i — which waits for every rank's MoE step i — does
+    # not hold back its MoE step i+1
+    s_moe = torch.cuda.Stream(dev) if plan.colocated else s
     stream_moe = s_moe.cuda_stream
     epoch = [0]
 
@@ -883,6 +884,9 @@ def main():
     ap.add_argument("--gate", action="store_true",
                     help="box: MoE-side gating (rows only cross NVLink; every MoE GPU runs "
                          "the router GEMM + top-k on the full step)")
+    ap.add_argument("--combine", default="push", choices=["push", "switch"],
+                    help="NVLS combine: partial sums pushed point to point (default) or "
+                         "summed by the NVSwitch (multimem.ld_reduce)")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls", "routed"],
                     help="box exchange for --gpus > 1 (auto: NVLS multicast when supported; "
                          "routed: rows only to the MoE GPUs their slots are scheduled on)")

@@ -263,6 +263,11 @@ janus_status janus_xfer_check(janus_ctx *ctx);
 /* Instrumentation: device address of this rank's received token rows
  * [max_tokens][d_h] bf16 in epoch's slot (MoE ranks: the dispatch target). */
 janus_status janus_xfer_recv_rows(const janus_ctx *ctx, uint64_t epoch, void **rows);
+/* NVLS transport's combine, on every rank: 0 (default) = each MoE rank
+ * pushes its partial sums point to point into the owners' regions and the
+ * owner adds them in instance order; 1 = the owner reads them summed by the
+ * NVSwitch (multimem.ld_reduce).  The dispatch stays multicast either way. */
+janus_status janus_xfer_set_combine(janus_ctx *ctx, int switch_reduce);
 /* Bound of every flag wait of this endpoint (default 20 s). */
 janus_status janus_xfer_set_timeout(janus_ctx *ctx, uint64_t timeout_ns);
 /* Same-process connect (all ranks' contexts in one process, on one or several

@@ -34,7 +34,7 @@ SYMBOLS = (
     "janus_moe_set_shared_split",
     "janus_xfer_configure_colocated", "janus_xfer_check", "janus_xfer_set_timeout",
     "janus_xfer_connect_local", "janus_xfer_set_transport", "janus_attn_route_async",
-    "janus_xfer_recv_rows",
+    "janus_xfer_recv_rows", "janus_xfer_set_combine",
 )
 
 
@@ -105,6 +105,7 @@ def _load() -> C.CDLL:
     L.janus_xfer_set_transport.argtypes = [vp, i32]
     L.janus_attn_route_async.argtypes = [vp, vp, vp, i64, u64, vp]
     L.janus_xfer_recv_rows.argtypes = [vp, u64, P(vp)]
+    L.janus_xfer_set_combine.argtypes = [vp, i32]
     return L
 
 

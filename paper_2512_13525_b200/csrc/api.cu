@@ -726,7 +726,7 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     // (P2P / routed, K5 fused with the NVLink transfer) — then the step's
     // status and the combine flag are published on every attention rank
     const janus::XferState &x = ctx->xfer;
-    if (x.mc) {
+    if (x.mc && x.mc_reduce) {
       e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
                                 reinterpret_cast<void *>(x.uc_va + x.mpart_off +
                                                          janus::xfer_slot(push_epoch) * x.mslot),
@@ -876,6 +876,14 @@ janus_status janus_xfer_set_transport(janus_ctx *ctx, int routed) {
     CK(cudaMemset(x.dmask, 0, sizeof(uint32_t) * 2 * x.L.ta_max));
   }
   x.transport = routed ? janus::kXferRouted : janus::kXferP2P;
+  return JANUS_OK;
+}
+
+janus_status janus_xfer_set_combine(janus_ctx *ctx, int switch_reduce) {
+  if (!ctx || !ctx->xfer.local) return fail(ctx, JANUS_ESTATE, "xfer: configure first");
+  if (switch_reduce != 0 && switch_reduce != 1)
+    return fail(ctx, JANUS_EINVAL, "xfer: combine mode must be 0 or 1");
+  ctx->xfer.mc_reduce = switch_reduce != 0;
   return JANUS_OK;
 }
 
@@ -1053,9 +1061,10 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, ui
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = janus::launch_wait(x, 1, epoch, s);
   if (e == cudaSuccess)
-    e = x.mc ? janus::launch_reduce_mc(x, d_out, first, Ta, epoch, s)
-             : janus::launch_reduce_partials(x, d_out, Ta, epoch, s);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, x.mc ? "reduce_mc_kernel" : "reduce_partials_kernel");
+    e = x.mc && x.mc_reduce ? janus::launch_reduce_mc(x, d_out, first, Ta, epoch, s)
+                            : janus::launch_reduce_partials(x, d_out, Ta, epoch, s);
+  if (e != cudaSuccess)
+    return cuda_fail(ctx, e, x.mc && x.mc_reduce ? "reduce_mc_kernel" : "reduce_partials_kernel");
   ctx->launches += 2;
   return JANUS_OK;
 }

@@ -185,6 +185,11 @@ struct XferState {
   // NVLS multicast transport (mc.cpp): the bulk rows / routing / partial sums
   // go through one multicast object; flags stay in the IPC regions above.
   bool mc = false, mc_bound = false;
+  // NVLS combine: false (default) -> the MoE ranks push partial sums point to
+  // point (K5 push mode) and the owner adds them; true -> multimem.ld_reduce
+  // in the switch.  Measured (profiles/r2): push 27-51 us vs switch 114-127 us
+  // at 1A+3E / 4 colocated, c2 shape.
+  bool mc_reduce = false;
   unsigned long long mc_handle = 0, mem_handle = 0;  // CUmemGenericAllocationHandle
   unsigned long long mc_va = 0, uc_va = 0;           // multicast / own-backing mappings
   size_t mc_bytes = 0, mc_gran = 0;

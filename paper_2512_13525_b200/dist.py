@@ -123,7 +123,9 @@ class JanusBox:
     (the reference's semantics, comm.hpp:12-14); ``routed`` sends a row only to
     the MoE ranks its slots are scheduled on — attention ranks then also need
     the replica map (``rmap``) to run the scheduler; ``auto`` = NVLS when every
-    rank supports it, else P2P.
+    rank supports it, else P2P.  ``combine`` (NVLS only): ``push`` (default) —
+    MoE ranks push their partial sums point to point; ``switch`` — the owner
+    reads them summed by the NVSwitch (multimem.ld_reduce).
 
     Multi-process (one rank per GPU): the constructor exchanges the CUDA IPC
     handles over torch.distributed.  One process driving every rank (e.g. all on
@@ -131,7 +133,7 @@ class JanusBox:
 
     def __init__(self, plan: BoxPlan, rank: int, max_tokens: int, d_hidden: int, top_k: int,
                  layer=None, device: int = 0, group=None, transport: str = "auto", rmap=None,
-                 _connect: bool = True):
+                 combine: str = "push", _connect: bool = True):
         if transport not in TRANSPORTS:
             raise ValueError(transport)
         self.plan, self.rank = plan, rank
@@ -179,6 +181,8 @@ class JanusBox:
             if all(every):
                 self._setup_multicast(dist, group)
                 self.transport = "nvls"
+                if combine == "switch":  # default: point-to-point push combine
+                    self._check(lib.janus_xfer_set_combine(self._ctx, 1))
             elif transport == "nvls":
                 raise JanusError(5, "xfer: NVLS multicast not supported on every rank")
 

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls", "routed"])
+    ap.add_argument("--combine", default="push", choices=["push", "switch"])
     ap.add_argument("--shared", action="store_true", help="add a shared expert (NVLS only)")
     ap.add_argument("--shared-split", action="store_true",
                     help="the shared expert split evenly over the MoE instances (implies --shared)")
@@ -78,7 +79,7 @@ def main():
         if layer is not None:
             layer.set_router(wr)
     box = JanusBox(plan, rank, T, d_h, k, layer=layer, device=local, transport=args.transport,
-                   rmap=rmap)
+                   rmap=rmap, combine=args.combine)
     orc = Oracle()
     from paper_2512_13525_b200.moe import expert_weights
     wcache = {}
@@ -177,7 +178,7 @@ def main():
     except Exception as ex_:  # noqa: BLE001
         result["check"] = str(ex_)
     os.makedirs(args.out, exist_ok=True)
-    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}_{args.inflight}{'s' if args.shared else ''}{'x' if args.shared_split else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}_rank{rank}.json"), "w") as f:
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}{args.combine}_{args.inflight}{'s' if args.shared else ''}{'x' if args.shared_split else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}_rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
     dist.destroy_process_group()

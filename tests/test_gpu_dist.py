@@ -45,6 +45,30 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
                 assert s["bad"] == 0, s
 
 
+@pytest.mark.parametrize("attn,moe", [(1, 3), (2, 2)])
+def test_box_exchange_nvls_switch_combine(attn, moe):
+    """NVLS dispatch with the in-switch combine (multimem.ld_reduce) instead of
+    the default point-to-point push, two steps in flight."""
+    if gpus() < attn + moe:
+        pytest.skip(f"needs {attn + moe} GPUs (one rank per GPU)")
+    out = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={attn + moe}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29950 + 10 * attn + moe), os.path.join(ROOT, "tests", "dist_worker.py"),
+           "--attn", str(attn), "--moe", str(moe), "--out", out, "--transport", "nvls",
+           "--combine", "switch", "--inflight", "2"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
+    assert len(res) == attn + moe
+    for r in res:
+        assert not r["timed_out"], r
+        assert r["check"] == "ok", r
+        if r["role"] in ("attention", "both"):
+            for s_ in r["steps"]:
+                assert s_["bad"] == 0, s_
+
+
 @pytest.mark.parametrize("flag", ["--shared", "--shared-split", "--gate"])
 def test_box_exchange_shared_expert_and_moe_side_gating(flag):
     """--shared: the shared expert in a box (MoE instance 0 adds it to its
