@@ -559,11 +559,17 @@ def run_ours(args):
 
 
 def run_box(args):
-    """N > 1: one NVLink box split into A attention + M MoE GPUs
-    (BoxPlan.for_gpus: 1A+1E, 1A+3E, 2A+6E).  Same c2 expert shape as N=1; the
-    replica map is the reference placement for M instances (maps/c2_m{M}).
-    Weak scaling in the MoE sub-group: T = tokens x M per step, so every MoE GPU
-    sees ~T*k/M = tokens*k slots, as the single GPU does at N=1."""
+    """N > 1: one NVLink box.  Default (``--box moe-only``): every GPU owns a
+    token shard AND is an MoE instance (the attention and MoE sub-groups are
+    the same N GPUs), routed transport — each token row crosses NVLink only to
+    the instances its slots are scheduled on.  ``--box split``: the paper's
+    disaggregated split into A attention + M MoE GPUs (BoxPlan.for_gpus: 1A+1E,
+    1A+3E, 2A+6E), NVLS multicast dispatch; its attention GPUs run no attention
+    math here, so its per-GPU figure carries A idle GPUs.  Same c2 expert shape
+    as N=1; the replica map is the reference placement for M instances
+    (maps/c2_m{M}).  Weak scaling in the MoE sub-group: T = tokens x M per
+    step, so every MoE GPU sees ~T*k/M = tokens*k slots, as the single GPU
+    does at N=1."""
     import ctypes as C
 
     import torch
@@ -579,6 +585,13 @@ def run_box(args):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     plan = BoxPlan.moe_only(ws) if args.box == "moe-only" else BoxPlan.for_gpus(ws)
+    # measured defaults (profiles/r2/box4): MoE-only box -> routed transport,
+    # push combine; split box -> NVLS dispatch, combine summed in the switch
+    # (one attention GPU would otherwise take M full partial pushes)
+    if args.transport == "default":
+        args.transport = "routed" if plan.colocated else "auto"
+    if args.combine == "default":
+        args.combine = "push" if plan.colocated else "switch"
     A, M = plan.n_attn, plan.n_moe
     T = args.tokens * M
     att, moe = plan.is_attention(rank), plan.is_moe(rank)
@@ -739,24 +752,24 @@ def run_box(args):
         gwd2 = [gwd, torch.empty_like(gwd)] if not args.gate else [None, None]
         out2 = [out, torch.empty_like(out)]
         h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        ev_in = [torch.cuda.Event(), torch.cuda.Event()]    # inputs of slot b landed
-        ev_used = [torch.cuda.Event(), torch.cuda.Event()]  # dispatch read slot b
         ev_out = [torch.cuda.Event(), torch.cuda.Event()]   # combine wrote out[b]
         ev_read = [torch.cuda.Event(), torch.cuda.Event()]  # D2H read out[b]
 
         def h2d_dispatch(i):
+            # the dispatch goes on the copy stream right behind its inputs'
+            # H2D, so the compute stream's combine of the previous step never
+            # queues behind a PCIe copy
             b = i & 1
             with torch.cuda.stream(h2d_s):
                 if i >= 2:
-                    h2d_s.wait_event(ev_used[b])
+                    # step i-2's combine done: every MoE rank has consumed that
+                    # exchange slot and its input buffer (epoch parity reuse)
+                    h2d_s.wait_event(ev_out[b])
                 xd2[b].copy_(xh, non_blocking=True)
                 if not args.gate:
                     exd2[b].copy_(exh[i % N_BATCHES], non_blocking=True)
                     gwd2[b].copy_(gwh, non_blocking=True)
-                ev_in[b].record(h2d_s)
-            s.wait_event(ev_in[b])
-            box.dispatch(xd2[b], exd2[b], gwd2[b], T, e0_ + i + 1, stream)
-            ev_used[b].record(s)
+                box.dispatch(xd2[b], exd2[b], gwd2[b], T, e0_ + i + 1, h2d_s.cuda_stream)
 
         h2d_dispatch(0)
         for i in range(args.steps):
@@ -876,7 +889,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--box", default="split", choices=["split", "moe-only"],
+    ap.add_argument("--box", default="moe-only", choices=["split", "moe-only"],
                     help="--gpus > 1: the paper's attention/MoE split (1 attention GPU per "
                          "4), or the MoE-only box (every GPU owns tokens and experts)")
     ap.add_argument("--shape", default="c2", choices=sorted(SHAPES),
@@ -884,10 +897,11 @@ def main():
     ap.add_argument("--gate", action="store_true",
                     help="box: MoE-side gating (rows only cross NVLink; every MoE GPU runs "
                          "the router GEMM + top-k on the full step)")
-    ap.add_argument("--combine", default="push", choices=["push", "switch"],
+    ap.add_argument("--combine", default="default", choices=["default", "push", "switch"],
                     help="NVLS combine: partial sums pushed point to point (default) or "
                          "summed by the NVSwitch (multimem.ld_reduce)")
-    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nvls", "routed"],
+    ap.add_argument("--transport", default="default",
+                    choices=["default", "auto", "p2p", "nvls", "routed"],
                     help="box exchange for --gpus > 1 (auto: NVLS multicast when supported; "
                          "routed: rows only to the MoE GPUs their slots are scheduled on)")
     args = ap.parse_args()

@@ -18,6 +18,8 @@
  *   janus_moe_layer[_async]<- moe_layer_latency's subject: the MoE layer the
  *                             reference only models (src/latency.cpp:17-32)
  *   janus_moe_layer_latency<- moesim::moe_layer_latency (latency.hpp:34-35)
+ *   janus_latency_layer    <- the same, calibrated to the measured layer
+ *                             (janus_latency_fit; sim.cpp:193-195 callers)
  *   janus_shard_tokens     <- StepTraffic token ownership (src/comm.cpp:76-81)
  * See INTEGRATION.md for the binding a maintainer adds on the reference side.
  */
@@ -298,6 +300,41 @@ janus_status janus_xfer_mc_join(janus_ctx *ctx, int fd);
 janus_status janus_xfer_mc_bind(janus_ctx *ctx);
 
 /* ---- model / workload --------------------------------------------------- */
+/* The MoE-layer latency model, calibrated.  The reference
+ * prices an instance as t_launch + max(A*W_e/beta, F(b)/pi) with
+ * W_e = 2*d_h*d_e*bpp and F(b) = 2*b*d_h*d_e (latency.cpp:17-24, types.hpp:42-44)
+ * and a layer as the max over instances with work (latency.cpp:26-32).  This
+ * model generalises it:
+ *   t = t_launch + (mem^p + comp^p)^(1/p),
+ *   mem = A * matrices*d_h*d_e*bytes_per_param / hbm_bandwidth,
+ *   comp = b * 2*flop_matrices*d_h*d_e / peak_flops;
+ * p <= 0 is the reference's max, matrices = 2 / flop_matrices = 1 its
+ * accounting (3 / 3: the SwiGLU expert this library computes).  Units:
+ * seconds, B/s, FLOP/s. */
+typedef struct {
+  double t_launch;
+  double hbm_bandwidth;
+  double peak_flops;
+  double p;
+  int matrices;        /* weight matrices streamed per activated expert */
+  int bytes_per_param;
+  int flop_matrices;   /* matrices multiplied per routed row */
+} janus_latency_model;
+/* One instance with `activated_experts` replicas and `routed_tokens` rows
+ * (0 when it has none); a layer: the max over instances with load > 0 — the
+ * replacement for moe_instance_latency / moe_layer_latency that
+ * DecodeEngine::eval_step calls (sim.cpp:193-195). */
+double janus_latency_instance(const janus_latency_model *m, int activated_experts,
+                              int64_t routed_tokens, int d_hidden, int d_expert);
+double janus_latency_layer(const janus_latency_model *m, int num_instances, const int32_t *load,
+                           const int64_t *routed_tokens, int d_hidden, int d_expert);
+/* host: fit t_launch, hbm_bandwidth, peak_flops and p (> 1) to n >= 4 measured
+ * points (activated experts, routed rows, seconds) — minimum mean squared
+ * relative error; `model` gives the start (and matrices / bytes_per_param,
+ * kept) and receives the fit; mean_abs_rel_err (optional) its residual. */
+janus_status janus_latency_fit(int n, const int32_t *activated, const int64_t *routed_tokens,
+                               const double *seconds, int d_hidden, int d_expert,
+                               janus_latency_model *model, double *mean_abs_rel_err);
 /* The reference roofline prediction (latency.cpp:17-32), kept for comparison
  * with measured layer times. */
 double janus_moe_layer_latency(int num_instances, const int32_t *load,

@@ -1,5 +1,6 @@
 // janus_moesim_compat.hpp — C++ drop-in for the reference moesim scheduling API
-// (include/moesim/aebs.hpp:63-71 and latency.hpp:34-35 in /root/reference/proj),
+// (include/moesim/aebs.hpp:63-71 and latency.hpp:34-35 in /root/reference/proj;
+// calibrated_moe_layer_latency for sim.cpp:193-195),
 // implemented over the C ABI in janus_b200.h.  Header-only; link
 // libjanus_b200.so.
 //
@@ -159,6 +160,22 @@ inline moesim::Assignment schedule_reference(const moesim::ActivationBatch& b,
 inline moesim::Assignment schedule_random(const moesim::ActivationBatch& b,
                                           const moesim::ReplicaMap& m, uint64_t seed) {
   return janus_detail::run(b, m, JANUS_POLICY_RANDOM, seed);
+}
+
+// latency.hpp:34-35, calibrated to the measured layer (janus_latency_fit): the
+// call DecodeEngine::eval_step makes (sim.cpp:193-195) with the reference's
+// InstanceLoad {activated_experts, routed_tokens} (latency.hpp:28-31).
+template <class InstanceLoadT>
+inline double calibrated_moe_layer_latency(const std::vector<InstanceLoadT>& loads, int d_hidden,
+                                           int d_expert, const janus_latency_model& model) {
+  std::vector<int32_t> load(loads.size());
+  std::vector<int64_t> routed(loads.size());
+  for (size_t g = 0; g < loads.size(); ++g) {
+    load[g] = static_cast<int32_t>(loads[g].activated_experts);
+    routed[g] = static_cast<int64_t>(loads[g].routed_tokens);
+  }
+  return janus_latency_layer(&model, static_cast<int>(loads.size()), load.data(), routed.data(),
+                             d_hidden, d_expert);
 }
 
 }  // namespace JANUS_COMPAT_NS

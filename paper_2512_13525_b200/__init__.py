@@ -9,6 +9,7 @@ from .moesim import (ActivationBatch, Assignment, InstanceLoad, ParseError,  # n
                      ReplicaMap, Scheduler, ValidationError, config_map,
                      derive_seed, dump_assignment, load_batch, load_replica_map,
                      load_replica_map_file, max_activated_load, moe_layer_latency, schedule,
-                     schedule_random, schedule_reference, shard_tokens)
+                     schedule_random, schedule_reference, shard_tokens,
+                     reference_latency_model, fit_latency_model, layer_latency)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

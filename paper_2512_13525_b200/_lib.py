@@ -34,8 +34,16 @@ SYMBOLS = (
     "janus_moe_set_shared_split",
     "janus_xfer_configure_colocated", "janus_xfer_check", "janus_xfer_set_timeout",
     "janus_xfer_connect_local", "janus_xfer_set_transport", "janus_attn_route_async",
-    "janus_xfer_recv_rows", "janus_xfer_set_combine",
+    "janus_xfer_recv_rows", "janus_xfer_set_combine", "janus_latency_instance",
+    "janus_latency_layer", "janus_latency_fit",
 )
+
+
+class LatencyModel(C.Structure):
+    """janus_latency_model (janus_b200.h)."""
+    _fields_ = [("t_launch", C.c_double), ("hbm_bandwidth", C.c_double),
+                ("peak_flops", C.c_double), ("p", C.c_double), ("matrices", C.c_int),
+                ("bytes_per_param", C.c_int), ("flop_matrices", C.c_int)]
 
 
 class JanusAssignment(C.Structure):
@@ -106,6 +114,11 @@ def _load() -> C.CDLL:
     L.janus_attn_route_async.argtypes = [vp, vp, vp, i64, u64, vp]
     L.janus_xfer_recv_rows.argtypes = [vp, u64, P(vp)]
     L.janus_xfer_set_combine.argtypes = [vp, i32]
+    L.janus_latency_instance.argtypes = [P(LatencyModel), i32, i64, i32, i32]
+    L.janus_latency_instance.restype = dbl
+    L.janus_latency_layer.argtypes = [P(LatencyModel), i32, vp, vp, i32, i32]
+    L.janus_latency_layer.restype = dbl
+    L.janus_latency_fit.argtypes = [i32, vp, vp, vp, i32, i32, P(LatencyModel), P(dbl)]
     return L
 
 

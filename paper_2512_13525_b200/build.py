@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libjanus_b200.so")
-SOURCES = ["api.cu", "aebs.cu", "gemm.cu", "ffn.cu", "xfer.cu", "gate.cu", "stats.cu", "mc.cpp"]
+SOURCES = ["api.cu", "aebs.cu", "gemm.cu", "ffn.cu", "xfer.cu", "gate.cu", "stats.cu", "mc.cpp", "latency.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

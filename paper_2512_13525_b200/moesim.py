@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ._lib import (EINVAL, EUNKNOWN_EXPERT, OK, POLICY_AEBS, POLICY_RANDOM, STATUS_NAMES,
-                   JanusAssignment, lib)
+                   JanusAssignment, LatencyModel, lib)
 
 MAPS_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "maps")
 
@@ -438,3 +438,39 @@ def shard_tokens(num_tokens: int, attn_instances: int, a: int):
     first, count = C.c_int64(), C.c_int64()
     lib.janus_shard_tokens(num_tokens, attn_instances, a, C.byref(first), C.byref(count))
     return first.value, count.value
+
+
+# ---------------------------------------------- calibrated latency model --
+
+def reference_latency_model(peak_flops: float = 989e12, hbm_bandwidth: float = 3.35e12,
+                            kernel_launch_overhead: float = 5e-6,
+                            bytes_per_param: int = 2) -> LatencyModel:
+    """The reference's model (latency.cpp:17-24) as a janus_latency_model:
+    two matrices, max of the memory and compute terms (p = 0)."""
+    return LatencyModel(kernel_launch_overhead, hbm_bandwidth, peak_flops, 0.0, 2,
+                        bytes_per_param, 1)
+
+
+def fit_latency_model(activated, routed_tokens, seconds, hidden_dim: int, expert_dim: int,
+                      start: LatencyModel | None = None, matrices: int = 3):
+    """Fit (t_launch, beta, pi, p) to measured layer times (janus_latency_fit).
+    Returns (model, mean absolute relative error)."""
+    A = np.ascontiguousarray(activated, np.int32)
+    b = np.ascontiguousarray(routed_tokens, np.int64)
+    t = np.ascontiguousarray(seconds, np.float64)
+    m = start if start is not None else LatencyModel(20e-6, 6.5e12, 1.4e15, 4.0, matrices, 2,
+                                                     matrices)
+    err = C.c_double()
+    st = lib.janus_latency_fit(len(A), _ptr(A), _ptr(b), _ptr(t), hidden_dim, expert_dim,
+                               C.byref(m), C.byref(err))
+    if st != OK:
+        raise JanusError(st, "latency fit: need >= 4 points with positive times")
+    return m, err.value
+
+
+def layer_latency(model: LatencyModel, loads, hidden_dim: int, expert_dim: int) -> float:
+    """max over instances of the (calibrated) instance time (janus_latency_layer)."""
+    load = np.array([l.activated_experts for l in loads], np.int32)
+    routed = np.array([l.routed_tokens for l in loads], np.int64)
+    return float(lib.janus_latency_layer(C.byref(model), len(load), _ptr(load), _ptr(routed),
+                                         hidden_dim, expert_dim))

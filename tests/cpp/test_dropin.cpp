@@ -13,6 +13,7 @@
 
 #include "moesim/aebs.hpp"
 #include "moesim/experts.hpp"
+#include "moesim/latency.hpp"
 #include "moesim/workload.hpp"
 #define JANUS_USE_REFERENCE_TYPES
 #include "janus_moesim_compat.hpp"
@@ -107,6 +108,20 @@ int main() {
     got = e.what();
   }
   CHECK(!want.empty() && want == got);
+  // the latency model with the reference's accounting is moe_layer_latency
+  // (latency.cpp:17-32) on the reference's own InstanceLoad / ModelSpec
+  {
+    ModelSpec ms;
+    ms.hidden_dim = 4096;
+    ms.expert_dim = 1536;
+    HardwareSpec hw;
+    std::vector<InstanceLoad> loads;
+    for (int g = 0; g < 6; ++g) loads.push_back(InstanceLoad{g * 7 % 23, (long long)g * 1337});
+    const janus_latency_model rm{hw.kernel_launch_overhead, hw.hbm_bandwidth, hw.peak_flops, 0.0,
+                                 2, ms.bytes_per_param, 1};
+    CHECK(janus::calibrated_moe_layer_latency(loads, ms.hidden_dim, ms.expert_dim, rm) ==
+          moe_layer_latency(loads, ms, hw));
+  }
   std::printf("test_dropin: %d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
 }

@@ -10,7 +10,7 @@ x 1.5).  Prints one JSON document: the grid, the reference's prediction with
 MEASURED_PEAKS (uncalibrated), and the fitted (t_launch, beta, pi) of the
 three-matrix form with its residuals.
 
-  python tools/calibrate_latency.py [--d-h 2048 --d-e 768 --out profiles/r1/latency_calibration.json]
+  python tools/calibrate_latency.py [--d-h 2048 --d-e 768 --out profiles/r2/latency_calibration.json]
 """
 import argparse
 import ctypes as C
@@ -71,38 +71,29 @@ def main():
             pts.append({"A": act, "b": T * k, "T": T, "us": t * 1e6})
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     beta0, pi0 = pk["hbm_gbs"] * 1e9, pk["bf16_tflops_sustained"] * 1e12
-    W2 = 2 * d_h * d_e * 2          # the reference's bytes per expert (2 matrices, bf16)
-    F2 = lambda b: 2.0 * b * d_h * d_e  # noqa: E731  reference FLOPs (2 per MAC, 1 matrix pair)
-    for p in pts:  # the reference model as shipped (t_launch 5 us), measured peaks
-        p["ref_model_us"] = 1e6 * (5e-6 + max(p["A"] * W2 / beta0, F2(p["b"]) / pi0))
-    # three-matrix form, fitted: t = t0 + max(A*1.5*W2/beta, 1.5*3*F2(b)/pi)... in
-    # SwiGLU terms: bytes 3*d_h*d_e*2 per expert, FLOPs 6*d_h*d_e per routed row
-    from scipy.optimize import least_squares
-    Av = np.array([p["A"] for p in pts], float)
-    bv = np.array([p["b"] for p in pts], float)
-    tv = np.array([p["us"] for p in pts], float) * 1e-6
-    W3, F3 = 3 * d_h * d_e * 2, 6.0 * d_h * d_e
-
-    def model(th):
-        t0, beta, pi = th
-        return t0 + np.maximum(Av * W3 / beta, bv * F3 / pi)
-
-    fit = least_squares(lambda th: (model(th) - tv) / tv, x0=[10e-6, beta0, pi0],
-                        bounds=([0, 1e11, 1e13], [1e-3, 2e13, 5e15]))
-    t0, beta, pi = fit.x
-    pred = model(fit.x)
-    for p, q in zip(pts, pred):
-        p["fit_us"] = q * 1e6
+    A = [p["A"] for p in pts]
+    b = [p["b"] for p in pts]
+    tv = np.array([p["us"] for p in pts]) * 1e-6
+    ref = J.reference_latency_model(pi0, beta0, 5e-6)  # the model as shipped, measured peaks
+    for p in pts:
+        p["ref_model_us"] = 1e6 * J.layer_latency(ref, [J.InstanceLoad(p["A"], p["b"])], d_h, d_e)
+    # the calibrated form through the C ABI (janus_latency_fit): SwiGLU
+    # accounting (3 weight matrices, 3 matrices of FLOPs per row), p-norm blend
+    m, err = J.fit_latency_model(A, b, tv, d_h, d_e)
+    for p in pts:
+        p["fit_us"] = 1e6 * J.layer_latency(m, [J.InstanceLoad(p["A"], p["b"])], d_h, d_e)
     res = {
         "shape": {"experts": E, "top_k": k, "d_hidden": d_h, "d_expert": d_e},
         "reference_model": {"form": "t_launch + max(A*2*d_h*d_e*bpp/beta, 2*b*d_h*d_e/pi) "
                                     "(latency.cpp:17-24), MEASURED_PEAKS",
                             "mean_abs_rel_err": float(np.mean(np.abs(
                                 np.array([p["ref_model_us"] for p in pts]) * 1e-6 - tv) / tv))},
-        "fitted_swiglu_model": {"form": "t0 + max(A*3*d_h*d_e*2/beta, b*6*d_h*d_e/pi)",
-                                "t0_us": t0 * 1e6, "beta_GBps": beta / 1e9,
-                                "pi_TFLOPs": pi / 1e12,
-                                "mean_abs_rel_err": float(np.mean(np.abs(pred - tv) / tv))},
+        "fitted_model": {"form": "t_launch + (mem^p + comp^p)^(1/p), mem = A*3*d_h*d_e*2/beta, "
+                                 "comp = b*6*d_h*d_e/pi (janus_latency_fit)",
+                         "t_launch_s": m.t_launch, "hbm_bandwidth_Bps": m.hbm_bandwidth,
+                         "peak_flops": m.peak_flops, "p": m.p, "matrices": m.matrices,
+                         "bytes_per_param": m.bytes_per_param, "flop_matrices": m.flop_matrices,
+                         "mean_abs_rel_err": err},
         "points": pts,
     }
     txt = json.dumps(res, indent=1)
