@@ -761,14 +761,16 @@ def run_box(args):
             # queues behind a PCIe copy
             b = i & 1
             with torch.cuda.stream(h2d_s):
-                if i >= 2:
-                    # step i-2's combine done: every MoE rank has consumed that
-                    # exchange slot and its input buffer (epoch parity reuse)
-                    h2d_s.wait_event(ev_out[b])
+                # input buffer b: free once dispatch(i-2) ran (earlier on this stream)
                 xd2[b].copy_(xh, non_blocking=True)
                 if not args.gate:
                     exd2[b].copy_(exh[i % N_BATCHES], non_blocking=True)
                     gwd2[b].copy_(gwh, non_blocking=True)
+                if i >= 2:
+                    # exchange slot of epoch parity b: free once step i-2's
+                    # combine completed (every MoE rank consumed it); the H2D
+                    # above already overlaps that step
+                    h2d_s.wait_event(ev_out[b])
                 box.dispatch(xd2[b], exd2[b], gwd2[b], T, e0_ + i + 1, h2d_s.cuda_stream)
 
         h2d_dispatch(0)

@@ -1047,7 +1047,16 @@ cudaError_t launch_variant(const SchedArgs &a, size_t smem, int csize, cudaStrea
   return cudaLaunchKernelEx(&cfg, aebs_schedule_kernel<MAXIT>, a);
 }
 
+__global__ void abort_gate_kernel(SchedArgs a) {
+  if (*a.abort_flag) write_error_layout(a, JANUS_EPEER, 0);
+}
+
 }  // namespace
+
+cudaError_t launch_abort_gate(const SchedArgs &a, cudaStream_t stream) {
+  abort_gate_kernel<<<1, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
 
 size_t schedule_smem_bytes(int E, int N, int R) {
   const size_t base = (size_t)N * 4 + (size_t)32 * E * 4 + (size_t)6 * E * 4 + (size_t)N * 4 +

@@ -185,6 +185,10 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->xfer.err);
   free_assign(ctx->xfer.rws);
   dfree(ctx->xfer.dmask);
+  for (int i = 0; i < 2; ++i) {
+    free_assign(ctx->xfer.lay[i]);
+    dfree(ctx->xfer.lay_tile[i]);
+  }
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -643,10 +647,22 @@ janus_status janus_moe_set_weights(janus_ctx *ctx, int instance, const void *w13
 // box exchange: K1 schedule -> K3 permute -> K4 GEMMs -> K5 combine, where
 // the combine either writes `d_out` locally or (push_epoch != 0) pushes this
 // instance's partial sums into the owning attention ranks' memory.
+// GEMM n-tile: decode steps (few rows per replica group) use 64-row tiles
+// and the deep 9-stage weight ring; larger steps 256-row tiles.
+// Crossover measured on the c2 shape (FFN µs, 64 vs 256-row tiles): 24 rows
+// per expert 194.5 vs 196.0, 32: 204.2 vs 200.9, 48: 218.5 vs 209.2.
+static int layer_tile_n(const janus_ctx *ctx, int T) {
+  return (int64_t)T * ctx->top_k <= 28LL * ctx->dmap.E ? 64 : janus::kTileN;
+}
+
+// pre / pre_tile (optional): this step's layout, computed earlier by the same
+// context's attention role (colocated routed box) — K1 is then not rerun.
 static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                               const float *d_gate_w, int T, void *d_out,
                               const janus_assignment *assign, cudaStream_t s,
-                              unsigned long long push_epoch, const int *abort_flag = nullptr) {
+                              unsigned long long push_epoch, const int *abort_flag = nullptr,
+                              const janus_assignment *pre = nullptr,
+                              int32_t *pre_tile = nullptr) {
   janus_status st = check_ready(ctx);
   if (st != JANUS_OK) return st;
   if (!ctx->moe_ready) return fail(ctx, JANUS_ESTATE, "moe: weights not set");
@@ -667,11 +683,12 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
     a.group_off = assign->group_off ? assign->group_off : a.group_off;
     a.status = assign->status ? assign->status : a.status;
   }
-  // GEMM n-tile: decode steps (few rows per replica group) use 64-row tiles
-  // and the deep 9-stage weight ring; larger steps 256-row tiles.
-  // Crossover measured on the c2 shape (FFN µs, 64 vs 256-row tiles): 24 rows
-  // per expert 194.5 vs 196.0, 32: 204.2 vs 200.9, 48: 218.5 vs 209.2.
-  ctx->ffn.tile_n = (int64_t)T * k <= 28LL * ctx->dmap.E ? 64 : janus::kTileN;
+  ctx->ffn.tile_n = layer_tile_n(ctx, T);
+  if (pre) {
+    a = *pre;
+    a.row_slot = nullptr;
+  }
+  int32_t *tile_off = pre ? pre_tile : ctx->ws_tile_off;
   cudaEvent_t *ev = nullptr;
   if (ctx->profiling) {
     const size_t need = 4 * (size_t)(ctx->prof_calls + 1);
@@ -702,10 +719,22 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
   const bool shared = sh1 > sh0;
   janus::FfnPlan &ps = ctx->ffn_shared;
   if (shared) ps.tile_n = sh1 - sh0 <= 64 ? 64 : janus::kTileN;
-  st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, ctx->ws_tile_off, s,
-                    shared ? ctx->shared_off : nullptr, shared ? ps.tile_n : 0, sh1 - sh0,
-                    abort_flag);
-  if (st != JANUS_OK) return st;
+  if (!pre) {
+    st = launch_sched(ctx, d_experts, T, k, JANUS_POLICY_AEBS, 0, a, tile_off, s,
+                      shared ? ctx->shared_off : nullptr, shared ? ps.tile_n : 0, sh1 - sh0,
+                      abort_flag);
+    if (st != JANUS_OK) return st;
+  } else if (abort_flag) {  // a shard never arrived: reject the precomputed layout
+    janus::SchedArgs g{};
+    g.S = T * k;
+    g.map = ctx->dmap;
+    g.out = a;
+    g.tile_off = tile_off;
+    g.abort_flag = abort_flag;
+    cudaError_t ge = janus::launch_abort_gate(g, s);
+    if (ge != cudaSuccess) return cuda_fail(ctx, ge, "abort_gate_kernel");
+    ctx->launches += 1;
+  }
   if (ev) CK(cudaEventRecord(ev[1], s));
   janus::FfnPlan &p = ctx->ffn;
   cudaError_t e = janus::launch_permute(d_x, a.slot_row, a.instance, ctx->instance, T * k, k,
@@ -714,7 +743,7 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
   if (e != cudaSuccess) return cuda_fail(ctx, e, "permute_kernel");
   int launches = 0;
   if (ev) CK(cudaEventRecord(ev[2], s));
-  e = janus::launch_ffn(p, a.group_off, ctx->ws_tile_off, s, &launches);
+  e = janus::launch_ffn(p, a.group_off, tile_off, s, &launches);
   if (e == cudaSuccess && shared)
     e = janus::launch_ffn(ps, ctx->shared_off, ctx->shared_off + 2, s, &launches);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "grouped_gemm_kernel");
@@ -812,6 +841,10 @@ static void xfer_release(janus_ctx *ctx) {
   dfree(x.err);
   free_assign(x.rws);
   dfree(x.dmask);
+  for (int i = 0; i < 2; ++i) {
+    free_assign(x.lay[i]);
+    dfree(x.lay_tile[i]);
+  }
   x = janus::XferState{};
   ctx->xfer_ready = false;
 }
@@ -874,6 +907,14 @@ janus_status janus_xfer_set_transport(janus_ctx *ctx, int routed) {
                     JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
     CK(dalloc(&x.dmask, 2 * x.L.ta_max));
     CK(cudaMemset(x.dmask, 0, sizeof(uint32_t) * 2 * x.L.ta_max));
+    if (x.moe0 == 0 && ctx->ffn.h) {  // colocated with a configured layer: one K1 per step
+      for (int i = 0; i < 2; ++i) {
+        CK(alloc_assign(x.lay[i], (int)std::min<long long>(x.T_max * x.k, INT_MAX),
+                        JANUS_MAX_EXPERTS, JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
+        CK(dalloc(&x.lay_tile[i], JANUS_MAX_REPLICAS + 1));
+        CK(cudaMemset(x.lay_tile[i], 0, sizeof(int32_t) * (JANUS_MAX_REPLICAS + 1)));
+      }
+    }
   }
   x.transport = routed ? janus::kXferRouted : janus::kXferP2P;
   return JANUS_OK;
@@ -1000,12 +1041,17 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
                                              x.L.ex_off + janus::xfer_slot(epoch) * x.L.slot_stride);
     abort_flag = x.err + janus::kErrSkip + 2;
   }
-  janus_assignment ra = x.rws;
-  ra.slot_row = ra.row_slot = ra.group_off = nullptr;
-  janus_status st = launch_sched(ctx, full, (int)T, x.k, JANUS_POLICY_AEBS, 0, ra, nullptr, s,
-                                 nullptr, 0, 0, abort_flag);
+  const int sl = (int)janus::xfer_slot(epoch);
+  const bool full_layout = x.lay[sl].instance != nullptr;  // colocated: the MoE role reuses it
+  janus_assignment ra = full_layout ? x.lay[sl] : x.rws;
+  ra.row_slot = nullptr;
+  if (!full_layout) ra.slot_row = ra.group_off = nullptr;
+  if (full_layout) ctx->ffn.tile_n = layer_tile_n(ctx, (int)T);
+  janus_status st = launch_sched(ctx, full, (int)T, x.k, JANUS_POLICY_AEBS, 0, ra,
+                                 full_layout ? x.lay_tile[sl] : nullptr, s, nullptr, 0, 0,
+                                 abort_flag);
   if (st != JANUS_OK) return st;
-  e = janus::launch_routed_dispatch(x, d_x, x.rws.instance, x.rws.status, T, epoch, s);
+  e = janus::launch_routed_dispatch(x, d_x, ra.instance, ra.status, T, epoch, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "routed_dispatch_kernel");
   ctx->launches += 1;
   return JANUS_OK;
@@ -1044,6 +1090,13 @@ janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoc
   }
   unsigned char *base =
       static_cast<unsigned char *>(x.local) + janus::xfer_slot(epoch) * x.L.slot_stride;
+  const int sl = (int)janus::xfer_slot(epoch);
+  if (x.transport == janus::kXferRouted && x.lay[sl].instance && !ctx->shared)
+    // this rank's own dispatch of the epoch (flagged before the wait above
+    // returned) computed the step's layout: no second K1
+    return layer_run(ctx, base + x.L.x_off, nullptr,
+                     reinterpret_cast<const float *>(base + x.L.gw_off), (int)T, nullptr, nullptr,
+                     s, epoch, abort_flag, &x.lay[sl], x.lay_tile[sl]);
   return layer_run(ctx, base + x.L.x_off, reinterpret_cast<const int32_t *>(base + x.L.ex_off),
                    reinterpret_cast<const float *>(base + x.L.gw_off), (int)T, nullptr, nullptr, s,
                    epoch, abort_flag);

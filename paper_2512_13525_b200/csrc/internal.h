@@ -69,6 +69,9 @@ inline int id_bits_for(int E) {
 
 // Launches the fused scheduler + layout kernel (aebs.cu).
 cudaError_t launch_schedule(const SchedArgs &a, cudaStream_t stream);
+// A layout computed earlier is used as is, unless *a.abort_flag: then the
+// error layout (JANUS_EPEER) is written over it (aebs.cu).
+cudaError_t launch_abort_gate(const SchedArgs &a, cudaStream_t stream);
 size_t schedule_smem_bytes(int E, int N, int R);
 
 // MoE FFN workspace (ffn.cu).
@@ -182,6 +185,11 @@ struct XferState {
   // epoch slot ([2][ta_max])
   janus_assignment rws{};
   uint32_t *dmask = nullptr;
+  // colocated routed ranks: the attention role's K1 writes the whole layout of
+  // the step per epoch slot, and the rank's MoE role runs on it (one K1 per
+  // step per GPU instead of two)
+  janus_assignment lay[2] = {};
+  int32_t *lay_tile[2] = {nullptr, nullptr};
   // NVLS multicast transport (mc.cpp): the bulk rows / routing / partial sums
   // go through one multicast object; flags stay in the IPC regions above.
   bool mc = false, mc_bound = false;
