@@ -37,6 +37,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -225,11 +226,6 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   const bool leader = crank == 0;  // writes the per-expert / per-instance outputs
   uint64_t *trace = leader ? a.trace : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
-  // the box exchange aborted this step (a peer never published its rows)
-  if (a.abort_flag && *a.abort_flag) {
-    if (leader) write_error_layout(a, JANUS_EPEER, 0);
-    return;  // before any cluster barrier: every CTA reads the same flag
-  }
 
   // routed counts fit 32 bits (S < 2^31): 32-bit shared atomics are native.
   unsigned *routed = reinterpret_cast<unsigned *>(smem);        // [N]
@@ -268,7 +264,6 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
   const int nit = (cwin + 31) / 32;  // windows per warp
   const int beg = min(cend, cbeg + warp * nit * 32), end = min(cend, beg + nit * 32);
   Slots<MAXIT> sl;
-  sl.load(a.experts, beg, end, lane, nit);
   {
     // the first element per thread of every map table: all loads go out
     // before any smem store (in order, a load -> store pair per table would
@@ -319,6 +314,16 @@ __global__ void __launch_bounds__(kSchedThreads, 1) aebs_schedule_kernel(SchedAr
       s_pbhi[e] = __ldg(a.map.pair_bhi + e);
     }
   }
+  // the map is constant across steps: staged above before the dependency wait
+  // (overlaps the previous kernel under programmatic dependent launch); the
+  // routing, the abort word and every output belong to the predecessors
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the box exchange aborted this step (a peer never published its rows)
+  if (a.abort_flag && *a.abort_flag) {
+    if (leader) write_error_layout(a, JANUS_EPEER, 0);
+    return;  // before any cluster barrier: every CTA reads the same flag
+  }
+  sl.load(a.experts, beg, end, lane, nit);
   for (int g = tid; g < N; g += kSchedThreads) {
     load[g] = 0;
     routed[g] = 0;
@@ -729,10 +734,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) aebs_small_kernel(SchedArgs 
     a.trace[0] = globaltimer();
     c0 = clock64();
   }
-  if (a.abort_flag && *a.abort_flag) {  // the box exchange aborted this step
-    write_error_layout(a, JANUS_EPEER, 0);
-    return;
-  }
   int4 *exi = reinterpret_cast<int4 *>(smem);                   // [E]
   int2 *rep = reinterpret_cast<int2 *>(exi + E);                // [R]
   int32_t *cnt = reinterpret_cast<int32_t *>(rep + R);          // [16][E]
@@ -759,16 +760,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) aebs_small_kernel(SchedArgs 
   __shared__ int32_t s_load[32];
   __shared__ int32_t s_bad;
 
-  // ---- one round trip: this warp's slots + the compact map tables ---------
+  // ---- the compact map tables (constant across steps: staged before the
+  // dependency wait, so under programmatic dependent launch this overlaps the
+  // previous kernel), then this warp's slots ---------------------------------
   const int per = ((S + kSmallWarps - 1) / kSmallWarps + 31) / 32 * 32;
   const int beg = min(S, warp * per), end = min(S, beg + per);
   const int nit = (end - beg + 31) / 32;
-  int v[kSmallMaxIt];
-#pragma unroll
-  for (int i = 0; i < kSmallMaxIt; ++i) {
-    const int sl = beg + i * 32 + lane;
-    v[i] = (i < nit && sl < end) ? __ldg(a.experts + sl) : 0;
-  }
   // Every global load of the first element per thread goes out before any
   // smem store: an in-order warp would otherwise stall on each load -> store
   // pair in turn (one L2 round trip per table instead of one in all).
@@ -821,6 +818,19 @@ __global__ void __launch_bounds__(kSmallThreads, 1) aebs_small_kernel(SchedArgs 
   for (int i = tid + kSmallThreads; i < N * W; i += kSmallThreads) {
     pin[i] = __ldg(a.map.pin_mask + i);
     hmk[i] = __ldg(a.map.host_mask + i);
+  }
+  // the step's inputs (routing, the exchange's abort word) and every output
+  // buffer belong to the predecessor kernels until they complete
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.abort_flag && *a.abort_flag) {  // the box exchange aborted this step
+    write_error_layout(a, JANUS_EPEER, 0);
+    return;
+  }
+  int v[kSmallMaxIt];
+#pragma unroll
+  for (int i = 0; i < kSmallMaxIt; ++i) {
+    const int sl = beg + i * 32 + lane;
+    v[i] = (i < nit && sl < end) ? __ldg(a.experts + sl) : 0;
   }
   if (tid < 32) s_load[tid] = 0;
   if (tid == 0) s_bad = INT_MAX;
@@ -1037,13 +1047,15 @@ cudaError_t launch_variant(const SchedArgs &a, size_t smem, int csize, cudaStrea
   cfg.blockDim = dim3(kSchedThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = sm100::pdl_enabled && !a.trace ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, aebs_schedule_kernel<MAXIT>, a);
 }
 
@@ -1105,8 +1117,17 @@ cudaError_t launch_schedule(const SchedArgs &a, cudaStream_t stream) {
                : a.id_bits == 7 ? aebs_small_kernel<7>
                : a.id_bits == 8 ? aebs_small_kernel<8>
                                 : aebs_small_kernel<0>;
-      k<<<1, kSmallThreads, smem, stream>>>(a);
-      return cudaGetLastError();
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(1);
+      cfg.blockDim = dim3(kSmallThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = sm100::pdl_enabled && !a.trace ? 1 : 0;
+      return cudaLaunchKernelEx(&cfg, k, a);
     }
   }
   const size_t smem = schedule_smem_bytes(a.map.E, a.map.N, a.map.R);
