@@ -834,12 +834,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) aebs_small_kernel(SchedArgs 
   }
   if (tid < 32) s_load[tid] = 0;
   if (tid == 0) s_bad = INT_MAX;
-  if (a.trace && tid == 0) a.trace[14] = (uint64_t)(clock64() - c0);
   __syncthreads();
-  if (a.trace && tid == 0) {
-    a.trace[1] = globaltimer();
-    a.trace[15] = (uint64_t)(clock64() - c0);
-  }
+  if (a.trace && tid == 0) a.trace[1] = globaltimer();
 
   // ---- pass 1: warp histogram + the activated set --------------------------
   __shared__ int32_t s_scan[64];
@@ -951,12 +947,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) aebs_small_kernel(SchedArgs 
       }
     }
   }
-  if (a.trace && tid == 32) a.trace[12] = (uint64_t)(clock64() - c0);  // warp 1 done
   __syncthreads();
-  if (a.trace && tid == 0) {
-    a.trace[4] = globaltimer();
-    a.trace[13] = (uint64_t)(clock64() - c0);
-  }
+  if (a.trace && tid == 0) a.trace[4] = globaltimer();
 
   // ---- finish the multi-replica experts the greedy placed (the others were
   // finished during the greedy), then the group offsets ----------------------

@@ -1462,10 +1462,6 @@ janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int 
   ctx->launches += 3;
   for (int i = 0; i < 7; ++i) ns[i] = (int64_t)(h[i] - h[0]);
   ns[7] = (int64_t)h[7];  // SM cycles of the pass (0 where not recorded)
-  if (std::getenv("JANUS_TRACE_DEBUG"))
-    fprintf(stderr, "trace cycles: stage %llu staged %llu list0 %llu list1 %llu loop %llu sync %llu\n",
-            (unsigned long long)h[14], (unsigned long long)h[15], (unsigned long long)h[8],
-            (unsigned long long)h[9], (unsigned long long)h[10], (unsigned long long)h[13]);
   return JANUS_OK;
 }
 
