@@ -85,7 +85,24 @@ struct GemmParams {
   int up_off;     // SWIGLU: row offset of the up projection (d_e)
   __nv_bfloat16 *out;
   int out_ld;     // elements per output row
+  // tile timeline (JANUS_GEMM_TRACE=1, tools/gemm_timeline.py): per tile
+  // [draw, MMA start, accumulator ready, epilogue done, smid | q << 16 |
+  // rows << 32 | m << 48, issuer at the tile queue, ns the issuer waited for
+  // stages | ns it waited for the queue << 32, issue done] (%globaltimer ns);
+  // nullptr = off
+  unsigned long long *trace;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 // Cluster-window address of the same smem variable in CTA `rank` of the cluster.
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
@@ -330,6 +347,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int t_next = 0;  // drawn one tile ahead; consumed after this tile
       if (leader && lane == 0) t_next = (int)atomicAdd(p.ctr, 1u);
       const TileCoord c = tile_coord(p, t);
+      if (p.trace && leader && lane == 0) {
+        p.trace[8 * t] = gtimer();
+        p.trace[8 * t + 4] = smid() | (unsigned long long)c.q << 16 |
+                             (unsigned long long)c.rows << 32 | (unsigned long long)c.m << 48;
+      }
       const uint32_t bbytes = 2u * kBK * 2;  // per token row of the pair
       const uint32_t bytes_pair = 2u * kATileBytes + bbytes * c.half;
       const int rowq = (c.q - p.q_begin) * p.m_per_q;
@@ -373,6 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int slot = 0;
       uint32_t tq_phase = 0;
       while (true) {
+        const unsigned long long t_q = p.trace ? gtimer() : 0;
         mbar_wait(&tq_full[slot], tq_phase);
         const int t = tq[slot];
         __syncwarp();
@@ -382,6 +405,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           tq_phase ^= 1;
         }
         if (t >= total) break;
+        unsigned long long t_wait = 0;  // trace: time spent waiting for stages
+        const unsigned long long t_read = p.trace ? gtimer() : 0;
         const TileCoord c = tile_coord(p, t);
         const bool wide = c.half_hi != 0;
         const uint32_t idesc = idesc_bf16_m256(2 * c.half);
@@ -390,9 +415,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tempty[use & 1], ((use >> 1) & 1) ^ 1);
         if (wide) mbar_wait(&tempty[(use + 1) & 1], (((use + 1) >> 1) & 1) ^ 1);
         tc_fence_after();
+        if (p.trace && lane == 0) {
+          p.trace[8 * t + 1] = gtimer();
+          p.trace[8 * t + 5] = t_q;
+        }
         if (!wide) {
           for (int kb = 0; kb < kblocks; ++kb) {
+            const unsigned long long w0 = p.trace ? gtimer() : 0;
             mbar_wait(&full[stage], phase);
+            if (p.trace) t_wait += gtimer() - w0;
             tc_fence_after();
             const uint32_t sa = smem_u32(stage_base + stage * kStageBytes);
             const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kATileBytes);
@@ -446,6 +477,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (wide) umma_commit_pair(&tfull[(use + 1) & 1]);
         }
         __syncwarp();
+        if (p.trace && lane == 0) {
+          p.trace[8 * t + 6] = t_wait | (t_read - t_q) << 32;
+          p.trace[8 * t + 7] = gtimer();
+        }
         use += wide ? 2 : 1;
       }
     }
@@ -527,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int acc = use & 1;
       mbar_wait(&tfull[acc], (use >> 1) & 1);
       tc_fence_after();
+      if (p.trace && leader && warp == 2 && lane == 0 && sub == 0) p.trace[8 * t + 2] = gtimer();
       const uint32_t d = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
       // accumulator column j <-> token row sr0 + j (CTA 0 loaded rows [0, half),
       // CTA 1 rows [half, 2*half) of the sub-tile)
@@ -605,6 +641,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // above) must precede the MMA's reuse of the accumulator; a release
       // arrive would also wait for this warp's global stores to be acked
       if (lane == 0) mbar_arrive_cluster_relaxed(acc ? tempty_leader1 : tempty_leader0);
+      if (p.trace && lane == 0) atomicMax(&p.trace[8 * t + 3], gtimer());  // last warp of the pair
       }
     }
   }
@@ -670,7 +707,17 @@ bool make_w13_map(CUtensorMap *tm, const void *base, uint64_t Q, uint64_t d_e, u
 
 }  // namespace
 
+namespace {
+constexpr int kTraceTiles = 1 << 14;  // per GEMM
+unsigned long long *g_trace = nullptr;
+}  // namespace
+
 cudaError_t build_ffn_tensor_maps(FfnPlan &p) {
+  // the tile-timeline buffer (debug), allocated here: never during a capture
+  static const bool trace = getenv("JANUS_GEMM_TRACE") && atoi(getenv("JANUS_GEMM_TRACE"));
+  if (trace && !g_trace &&
+      cudaMalloc(&g_trace, 2ull * kTraceTiles * 8 * sizeof(unsigned long long)) != cudaSuccess)
+    return cudaErrorMemoryAllocation;
   const int Q = p.q_end - p.q_begin;
   bool ok = make_w13_map(&p.tm_w13, p.w13, Q, p.d_e, p.d_h) &&
             make_map(&p.tm_w2, p.w2, (uint64_t)Q * p.d_h, p.d_e, 128);
@@ -710,6 +757,7 @@ cudaError_t launch_gemm(const GemmParams &g, cudaStream_t s) {
 cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
                        cudaStream_t s, int *launches) {
   GemmParams g{};
+  g.trace = g_trace;
   g.group_off = group_off;
   g.tile_off = tile_off;
   g.tile_n = p.tile_n;
@@ -742,9 +790,20 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   g.up_off = 0;
   g.out = reinterpret_cast<__nv_bfloat16 *>(p.y);
   g.out_ld = p.d_h;
+  if (g.trace) g.trace += (size_t)kTraceTiles * 8;
   err = decode ? launch_gemm<kPlain, 32>(g, s) : launch_gemm<kPlain, 128>(g, s);
   if (launches) *launches += 2;
   return err;
 }
 
 }  // namespace janus
+
+// Debug: copy the traced FFN tile timeline ([2 GEMMs][16384 tiles][8] u64) to
+// host and clear it; JANUS_ESTATE when JANUS_GEMM_TRACE was not set.
+extern "C" int janus_debug_ffn_trace(unsigned long long *host, int cap_words) {
+  if (!janus::g_trace) return 4;
+  const size_t n = std::min((size_t)cap_words, (size_t)2 * janus::kTraceTiles * 8);
+  if (cudaMemcpy(host, janus::g_trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 3;
+  // cleared after the read: the next read holds only tiles drawn after this one
+  return cudaMemset(janus::g_trace, 0, 2ull * janus::kTraceTiles * 64) == cudaSuccess ? 0 : 3;
+}
