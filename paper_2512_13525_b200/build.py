@@ -28,6 +28,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
            f"-I{os.path.join(ROOT, 'include')}", "-o", LIB,
+           *os.environ.get("JANUS_NVCC_FLAGS", "").split(),  # experiments: -D overrides
            *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

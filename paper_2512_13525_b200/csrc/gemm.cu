@@ -93,6 +93,9 @@ struct GemmParams {
   unsigned long long *trace;
 };
 
+constexpr int kTW = 16;               // trace words per tile
+constexpr int kTraceTiles = 1 << 14;  // per GEMM; the last 512 tiles' words: CTA 0's stage log
+constexpr size_t kStageLog = (size_t)(kTraceTiles - 512) * kTW;  // [2048 stages][A, B, full, rows]
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -317,6 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ============ weight (A) producer + tile fetch (both CTAs) ============
     const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+    int nst = 0;  // trace: stages so far
     int stage = 0;
     uint32_t phase = 0;
     int slot = 0;
@@ -348,15 +352,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       if (leader && lane == 0) t_next = (int)atomicAdd(p.ctr, 1u);
       const TileCoord c = tile_coord(p, t);
       if (p.trace && leader && lane == 0) {
-        p.trace[8 * t] = gtimer();
-        p.trace[8 * t + 4] = smid() | (unsigned long long)c.q << 16 |
+        p.trace[kTW * t] = gtimer();
+        p.trace[kTW * t + 4] = smid() | (unsigned long long)c.q << 16 |
                              (unsigned long long)c.rows << 32 | (unsigned long long)c.m << 48;
       }
       const uint32_t bbytes = 2u * kBK * 2;  // per token row of the pair
       const uint32_t bytes_pair = 2u * kATileBytes + bbytes * c.half;
       const int rowq = (c.q - p.q_begin) * p.m_per_q;
+      const unsigned long long a0 = p.trace ? gtimer() : 0;
+      unsigned long long a_acq = 0;
       for (int kb = 0; kb < kblocks; ++kb) {
+        const unsigned long long w0 = p.trace ? gtimer() : 0;
         mbar_wait(&empty[stage], phase ^ 1);
+        if (p.trace) {
+          const unsigned long long w1 = gtimer();
+          a_acq += w1 - w0;
+          if (blockIdx.x == 0 && lane == 0 && nst < 2048) p.trace[kStageLog + 4 * nst] = w1;
+          ++nst;
+        }
         unsigned char *sa = stage_base + stage * kStageBytes;
         const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
         if (elect_one()) {
@@ -384,12 +397,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
+      if (p.trace && leader && lane == 0) {
+        p.trace[kTW * t + 8] = a_acq;
+        p.trace[kTW * t + 9] = gtimer() - a0;
+      }
       t = __shfl_sync(0xffffffffu, t_next, 0);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
     if (leader) {
-      int stage = 0;
+      int stage = 0, nst = 0;
       uint32_t phase = 0;
       uint32_t use = 0;  // accumulator uses so far: buffer use&1, phase (use>>1)&1
       int slot = 0;
@@ -416,14 +433,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (wide) mbar_wait(&tempty[(use + 1) & 1], (((use + 1) >> 1) & 1) ^ 1);
         tc_fence_after();
         if (p.trace && lane == 0) {
-          p.trace[8 * t + 1] = gtimer();
-          p.trace[8 * t + 5] = t_q;
+          p.trace[kTW * t + 1] = gtimer();
+          p.trace[kTW * t + 5] = t_q;
         }
         if (!wide) {
           for (int kb = 0; kb < kblocks; ++kb) {
             const unsigned long long w0 = p.trace ? gtimer() : 0;
             mbar_wait(&full[stage], phase);
-            if (p.trace) t_wait += gtimer() - w0;
+            if (p.trace) {
+              const unsigned long long w1 = gtimer();
+              t_wait += w1 - w0;
+              if (blockIdx.x == 0 && lane == 0 && nst < 2048) p.trace[kStageLog + 4 * nst + 2] = w1;
+              ++nst;
+            }
             tc_fence_after();
             const uint32_t sa = smem_u32(stage_base + stage * kStageBytes);
             const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kATileBytes);
@@ -478,8 +500,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         __syncwarp();
         if (p.trace && lane == 0) {
-          p.trace[8 * t + 6] = t_wait | (t_read - t_q) << 32;
-          p.trace[8 * t + 7] = gtimer();
+          p.trace[kTW * t + 6] = t_wait | (t_read - t_q) << 32;
+          p.trace[kTW * t + 7] = gtimer();
         }
         use += wide ? 2 : 1;
       }
@@ -490,7 +512,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // cost of one warp was measurable on the critical path.
     {
       const uint64_t pol_x = policy_evict_last();  // token rows: reused by every m-block
-      int stage = 0;
+      int stage = 0, nst = 0;
       uint32_t phase = 0;
       int slot = 0;
       uint32_t tq_phase = 0;
@@ -505,11 +527,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         if (t >= total) break;
         const TileCoord c = tile_coord(p, t);
+        const unsigned long long b0 = p.trace ? gtimer() : 0;
+        unsigned long long b_acq = 0;
         for (int kb = 0; kb < kblocks; ++kb) {
           for (int sub = 0; sub < (c.half_hi ? 2 : 1); ++sub) {
             const int half = sub ? c.half_hi : c.half;
             const int brow = c.r0 + sub * p.tile_n + (int)crank * half;
+            const unsigned long long w0 = p.trace ? gtimer() : 0;
             mbar_wait(&empty[stage], phase ^ 1);
+            if (p.trace) {
+              const unsigned long long w1 = gtimer();
+              b_acq += w1 - w0;
+              if (blockIdx.x == 0 && lane == 0 && nst < 2048) {
+                p.trace[kStageLog + 4 * nst + 1] = w1;
+                p.trace[kStageLog + 4 * nst + 3] = c.half + c.half_hi;
+              }
+              ++nst;
+            }
             unsigned char *sb = stage_base + stage * kStageBytes + kATileBytes;
             const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
             if (elect_one()) {
@@ -530,6 +564,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               phase ^= 1;
             }
           }
+        }
+        if (p.trace && leader && lane == 0) {
+          p.trace[kTW * t + 10] = b_acq;
+          p.trace[kTW * t + 11] = gtimer() - b0;
         }
       }
     }
@@ -562,7 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int acc = use & 1;
       mbar_wait(&tfull[acc], (use >> 1) & 1);
       tc_fence_after();
-      if (p.trace && leader && warp == 2 && lane == 0 && sub == 0) p.trace[8 * t + 2] = gtimer();
+      if (p.trace && leader && warp == 2 && lane == 0 && sub == 0) p.trace[kTW * t + 2] = gtimer();
       const uint32_t d = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
       // accumulator column j <-> token row sr0 + j (CTA 0 loaded rows [0, half),
       // CTA 1 rows [half, 2*half) of the sub-tile)
@@ -641,7 +679,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // above) must precede the MMA's reuse of the accumulator; a release
       // arrive would also wait for this warp's global stores to be acked
       if (lane == 0) mbar_arrive_cluster_relaxed(acc ? tempty_leader1 : tempty_leader0);
-      if (p.trace && lane == 0) atomicMax(&p.trace[8 * t + 3], gtimer());  // last warp of the pair
+      if (p.trace && lane == 0) atomicMax(&p.trace[kTW * t + 3], gtimer());  // last warp of the pair
       }
     }
   }
@@ -708,7 +746,6 @@ bool make_w13_map(CUtensorMap *tm, const void *base, uint64_t Q, uint64_t d_e, u
 }  // namespace
 
 namespace {
-constexpr int kTraceTiles = 1 << 14;  // per GEMM
 unsigned long long *g_trace = nullptr;
 }  // namespace
 
@@ -716,7 +753,7 @@ cudaError_t build_ffn_tensor_maps(FfnPlan &p) {
   // the tile-timeline buffer (debug), allocated here: never during a capture
   static const bool trace = getenv("JANUS_GEMM_TRACE") && atoi(getenv("JANUS_GEMM_TRACE"));
   if (trace && !g_trace &&
-      cudaMalloc(&g_trace, 2ull * kTraceTiles * 8 * sizeof(unsigned long long)) != cudaSuccess)
+      cudaMalloc(&g_trace, 2ull * kTraceTiles * kTW * sizeof(unsigned long long)) != cudaSuccess)
     return cudaErrorMemoryAllocation;
   const int Q = p.q_end - p.q_begin;
   bool ok = make_w13_map(&p.tm_w13, p.w13, Q, p.d_e, p.d_h) &&
@@ -790,7 +827,7 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   g.up_off = 0;
   g.out = reinterpret_cast<__nv_bfloat16 *>(p.y);
   g.out_ld = p.d_h;
-  if (g.trace) g.trace += (size_t)kTraceTiles * 8;
+  if (g.trace) g.trace += (size_t)kTraceTiles * kTW;
   err = decode ? launch_gemm<kPlain, 32>(g, s) : launch_gemm<kPlain, 128>(g, s);
   if (launches) *launches += 2;
   return err;
@@ -798,12 +835,12 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
 
 }  // namespace janus
 
-// Debug: copy the traced FFN tile timeline ([2 GEMMs][16384 tiles][8] u64) to
+// Debug: copy the traced FFN tile timeline ([2 GEMMs][16384 tiles][16] u64) to
 // host and clear it; JANUS_ESTATE when JANUS_GEMM_TRACE was not set.
 extern "C" int janus_debug_ffn_trace(unsigned long long *host, int cap_words) {
   if (!janus::g_trace) return 4;
-  const size_t n = std::min((size_t)cap_words, (size_t)2 * janus::kTraceTiles * 8);
+  const size_t n = std::min((size_t)cap_words, (size_t)2 * janus::kTraceTiles * janus::kTW);
   if (cudaMemcpy(host, janus::g_trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 3;
   // cleared after the read: the next read holds only tiles drawn after this one
-  return cudaMemset(janus::g_trace, 0, 2ull * janus::kTraceTiles * 64) == cudaSuccess ? 0 : 3;
+  return cudaMemset(janus::g_trace, 0, 2ull * janus::kTraceTiles * janus::kTW * 8) == cudaSuccess ? 0 : 3;
 }

@@ -21,6 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 TRACE_TILES = 1 << 14
+TW = 16  # trace words per tile
 
 
 def analyse(tr, K, name, hbm, tf, pairs):
@@ -76,7 +77,9 @@ def analyse(tr, K, name, hbm, tf, pairs):
     # stage (data) waits, the rest = issuing
     acc_wait = (mma - tq) / 1e3 - tq_wait
     issue_span = (issued - mma) / 1e3
-    res = {"gemm": name, "tiles": int(len(tr)), "span_us": span,
+    prod = {"A_acquire": float(tr[:, 8].sum() / 1e3 / pairs), "A_loop": float(tr[:, 9].sum() / 1e3 / pairs),
+            "B_acquire": float(tr[:, 10].sum() / 1e3 / pairs), "B_loop": float(tr[:, 11].sum() / 1e3 / pairs)}
+    res = {"gemm": name, "tiles": int(len(tr)), "span_us": span, "producer_pair_us": prod,
            "issuer_pair_us": {"tile_queue_wait": float(tq_wait.sum() / pairs),
                               "acc_free_wait": float(acc_wait.sum() / pairs),
                               "stage_wait": float(wait.sum() / pairs),
@@ -120,7 +123,7 @@ def main():
     fn = lib.janus_debug_ffn_trace
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
     fn.restype = ctypes.c_int
-    buf = np.zeros(2 * TRACE_TILES * 8, dtype=np.uint64)
+    buf = np.zeros(2 * TRACE_TILES * TW, dtype=np.uint64)
     assert fn(buf.ctypes.data, buf.size) == 0  # read + clear the warm-up steps' stamps
     # one more step, after an L2 flush, then read its timeline
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -128,11 +131,12 @@ def main():
     layer.forward(x, batches[0], gw, out=out)
     torch.cuda.synchronize()
     assert fn(buf.ctypes.data, buf.size) == 0
-    buf = buf.reshape(2, TRACE_TILES, 8)
+    buf = buf.reshape(2, TRACE_TILES, TW)
     hbm, tf, _, _ = bench.peaks()
     pairs = torch.cuda.get_device_properties(0).multi_processor_count // 2
-    r1, (a0, a1) = analyse(buf[0], bench.D_H, "gate_up", hbm, tf, pairs)
-    r2, (b0, b1) = analyse(buf[1], bench.D_E, "down", hbm, tf, pairs)
+    nt = TRACE_TILES - 512  # the rest: stage log of CTA 0
+    r1, (a0, a1) = analyse(buf[0][:nt], bench.D_H, "gate_up", hbm, tf, pairs)
+    r2, (b0, b1) = analyse(buf[1][:nt], bench.D_E, "down", hbm, tf, pairs)
     res = {"T": T, "step_gemm_span_us": (b1 - a0) / 1e3, "gap_us": (b0 - a1) / 1e3,
            "overlap_note": "gap < 0: the down GEMM's first draw precedes gate/up's last epilogue (PDL)",
            "gemms": [r1, r2]}

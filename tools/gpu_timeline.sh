@@ -10,7 +10,7 @@ import sys,json
 for l in sys.stdin:
     if l.startswith('{'):
         d=json.loads(l); print('gemm span %.1f gap %.2f'%(d['step_gemm_span_us'], d['gap_us']))
-        for g in d['gemms']: print(' ', g['gemm'], 'span %.1f'%g['span_us'], {k:round(v,1) for k,v in g['issuer_pair_us'].items()}, 'tail %.1f'%g['tail_idle_us_mean'])
+        for g in d['gemms']: print(' ', g['gemm'], 'span %.1f'%g['span_us'], {k:round(v,1) for k,v in g['issuer_pair_us'].items()}, {k:round(v,1) for k,v in g['producer_pair_us'].items()}, 'tail %.1f'%g['tail_idle_us_mean'])
     else: print(l.rstrip())"
   for i in 1 2; do timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu 2>/dev/null | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('  value %.3fM ffn_us %.1f hbm %.3f'%(d['value']/1e6, r['ffn_us_per_step'], r['hbm_frac']), d['clocks']['sm_mhz'])"; done
