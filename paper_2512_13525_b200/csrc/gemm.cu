@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include "internal.h"
@@ -122,17 +123,25 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
 }
-// Publish a 32-bit value into a CTA's smem and complete that CTA's mbarrier
-// phase with it (arrive + expect 4 bytes, then st.async completing them): no
+// Publish a 16-byte record into a CTA's smem and complete that CTA's mbarrier
+// phase with it (arrive + expect 16 bytes, then st.async completing them): no
 // release fence, so the issuing thread does not wait for its in-flight TMA.
-__device__ __forceinline__ void publish_u32(uint32_t cl_dst, uint32_t v, uint32_t cl_bar) {
-  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], 4;" ::"r"(
+__device__ __forceinline__ void publish_v4(uint32_t cl_dst, int4 v, uint32_t cl_bar) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], 16;" ::"r"(
                    cl_bar)
                : "memory");
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
-                   cl_dst),
-               "r"(v), "r"(cl_bar)
-               : "memory");
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::
+          "r"(cl_dst),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(cl_bar)
+      : "memory");
+}
+__device__ __forceinline__ int4 ld_shared_v4(const void *p) {
+  int4 v;
+  asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
 }
 // Relaxed arrive (consumers of the tile queue: only "read before reuse").
 __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
@@ -217,36 +226,41 @@ struct TileCoord {
 
 __device__ __forceinline__ int rows_per_cta(int rows) { return (((rows + 1) >> 1) + 7) & ~7; }
 
-// Tile t (relative to the first tile of q_begin) -> (group, m-block, rows).
-// Group-major, n-tiles fastest (consecutive tiles share the weight block),
-// walked zig-zag (below).  The n-tile count per group comes from K2
-// (tile_off): ceil(r / tile_n), or in decode (merge_tail) max(1, r / tile_n)
-// with the last tile also taking the remainder — up to 2*tile_n - 1 rows, a
-// "wide" tile of two sub-tiles sharing every weight k-block, so a remainder
-// never costs its own pass over the weights.
-__device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in) {
-  const int base = p.tile_off[p.q_begin];
-  // draws alternate between the front and the back of the list: replica order
-  // follows placement order (hot experts first, experts.cpp place_replicas), so
-  // tensor-bound hot tiles and weight-streaming cold tiles run side by side
-  // (c2, T=4096: 334 -> 329 us)
-  const int total = (p.tile_off[p.q_end] - base) * p.m_tiles;
-  const int t = (t_in & 1) ? total - 1 - (t_in >> 1) : (t_in >> 1);
-  int lo = p.q_begin, hi = p.q_end;  // find q: (tile_off[q]-base)*m <= t < (tile_off[q+1]-base)*m
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if ((p.tile_off[mid] - base) * p.m_tiles <= t) lo = mid;
-    else hi = mid;
-  }
-  const int q = lo;
-  const int nt = p.tile_off[q + 1] - p.tile_off[q];
-  const int local = t - (p.tile_off[q] - base) * p.m_tiles;
+
+// Tiles are group-major, n-tiles fastest (consecutive tiles share the weight
+// block); the n-tile count per group comes from K2 (tile_off): ceil(r / tile_n),
+// or in decode (merge_tail) max(1, r / tile_n) with the last tile also taking
+// the remainder — up to 2*tile_n - 1 rows, a "wide" tile of two sub-tiles
+// sharing every weight k-block, so a remainder never costs its own pass over
+// the weights.
+// Token rows one CTA loads per stage for `half` rows: at most two TMA boxes
+// (each TMA issue is on the token producer's critical path) — the largest
+// power-of-two box <= half, then the remainder rounded up to a power of two.
+// Rows past `half` land in smem the MMA never reads.  Box index i = 8 << i rows.
+struct BBoxes {
+  int i0, i1;  // i1 < 0: one box
+  int rows;    // rows loaded (>= half)
+};
+__device__ __forceinline__ BBoxes b_boxes(int half) {
+  BBoxes b;
+  const int m8 = half >> 3;
+  b.i0 = 31 - __clz(m8);
+  const int rem = m8 - (1 << b.i0);
+  b.i1 = rem ? 32 - __clz(rem - 1) : -1;  // ceil(log2(rem))
+  b.rows = (8 << b.i0) + (rem ? 8 << b.i1 : 0);
+  return b;
+}
+
+// The tile record the leader's producer publishes through the tile queue:
+// {t, q, r0, rows | m << 16}; every other role rebuilds the TileCoord from it
+// with a few integer ops instead of a search over tile_off (a chain of
+// dependent L2 loads, ~1 us at every tile start in every role).
+__device__ __forceinline__ TileCoord coord_of(const GemmParams &p, const int4 rec) {
   TileCoord c;
-  c.q = q;
-  c.m = local / nt;
-  const int n = local % nt;
-  c.r0 = p.group_off[q] + n * p.tile_n;
-  c.rows = n == nt - 1 ? p.group_off[q + 1] - c.r0 : p.tile_n;
+  c.q = rec.y;
+  c.r0 = rec.z;
+  c.rows = rec.w & 0xFFFF;
+  c.m = rec.w >> 16;
   if (c.rows > p.tile_n) {
     c.half = p.tile_n >> 1;
     c.half_hi = rows_per_cta(c.rows - p.tile_n);
@@ -255,6 +269,39 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams &p, int t_in) {
     c.half_hi = 0;
   }
   return c;
+}
+
+// Tile t -> its record (warp-cooperative): the group is found by counting the tile_off
+// prefix entries <= t with all lanes (one round of independent loads), then
+// four lanes load the group's bounds.  Returns the record (all lanes).
+__device__ __forceinline__ int4 tile_locate(const GemmParams &p, int t_in, int total, int lane) {
+  if (t_in >= total) return make_int4(t_in, 0, 0, 0);
+  const int base = p.tile_off[p.q_begin];
+  // draws alternate between the front and the back of the list: replica order
+  // follows placement order (hot experts first, experts.cpp place_replicas), so
+  // tensor-bound hot tiles and weight-streaming cold tiles run side by side
+  const int t = (t_in & 1) ? total - 1 - (t_in >> 1) : (t_in >> 1);
+  int q = p.q_begin;
+  for (int j0 = p.q_begin + 1; j0 < p.q_end; j0 += 128) {
+    int v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + 32 * u + lane;
+      v[u] = j < p.q_end ? (p.tile_off[j] - base) * p.m_tiles : INT_MAX;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q += __popc(__ballot_sync(0xffffffffu, v[u] <= t));
+  }
+  int w = 0;  // lanes 0..3: tile_off[q], tile_off[q+1], group_off[q], group_off[q+1]
+  if (lane < 4) w = lane < 2 ? p.tile_off[q + lane] : p.group_off[q + lane - 2];
+  const int to0 = __shfl_sync(0xffffffffu, w, 0), to1 = __shfl_sync(0xffffffffu, w, 1);
+  const int g0 = __shfl_sync(0xffffffffu, w, 2), g1 = __shfl_sync(0xffffffffu, w, 3);
+  const int nt = to1 - to0;
+  const int local = t - (to0 - base) * p.m_tiles;
+  const int m = local / nt, n = local % nt;
+  const int r0 = g0 + n * p.tile_n;
+  const int rows = n == nt - 1 ? g1 - r0 : p.tile_n;
+  return make_int4(t_in, q, r0, rows | m << 16);
 }
 
 template <int MODE, int BH>
@@ -275,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint64_t *tq_full = bars + 2 * kStages + 4;  // [kTQ]   both: tile index published
   uint64_t *tq_empty = tq_full + kTQ;          // [kTQ]   leader: every consumer read it
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tq_empty + kTQ);
-  volatile int *tq = reinterpret_cast<volatile int *>(tmem_holder + 4);  // [kTQ]
+  int4 *tq = reinterpret_cast<int4 *>(tmem_holder + 4);  // [kTQ] tile records (16-B aligned)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
@@ -325,21 +372,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     int slot = 0;
     uint32_t tq_phase = 0;
-    int t = 0;
-    if (leader && lane == 0) t = (int)atomicAdd(p.ctr, 1u);
-    t = __shfl_sync(0xffffffffu, t, 0);
+    int4 rec = make_int4(0, 0, 0, 0);
+    if (leader) {
+      int t0 = 0;
+      if (lane == 0) t0 = (int)atomicAdd(p.ctr, 1u);
+      rec = tile_locate(p, __shfl_sync(0xffffffffu, t0, 0), total, lane);
+    }
     while (true) {
       if (leader) {
         mbar_wait(&tq_empty[slot], tq_phase ^ 1);
         if (elect_one()) {
-          const uint32_t dst = smem_u32((const void *)&tq[slot]), bar = smem_u32(&tq_full[slot]);
-          publish_u32(mapa(dst, 0), (uint32_t)t, mapa(bar, 0));
-          publish_u32(mapa(dst, 1), (uint32_t)t, mapa(bar, 1));
+          const uint32_t dst = smem_u32(&tq[slot]), bar = smem_u32(&tq_full[slot]);
+          publish_v4(mapa(dst, 0), rec, mapa(bar, 0));
+          publish_v4(mapa(dst, 1), rec, mapa(bar, 1));
         }
         __syncwarp();
       } else {
         mbar_wait(&tq_full[slot], tq_phase);
-        t = tq[slot];
+        rec = ld_shared_v4(&tq[slot]);
         __syncwarp();
         if (elect_one()) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
       }
@@ -347,17 +397,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         slot = 0;
         tq_phase ^= 1;
       }
+      const int t = rec.x;
       if (t >= total) break;
-      int t_next = 0;  // drawn one tile ahead; consumed after this tile
+      int t_next = 0;  // drawn one tile ahead; located after this tile's loads
       if (leader && lane == 0) t_next = (int)atomicAdd(p.ctr, 1u);
-      const TileCoord c = tile_coord(p, t);
+      const TileCoord c = coord_of(p, rec);
       if (p.trace && leader && lane == 0) {
         p.trace[kTW * t] = gtimer();
         p.trace[kTW * t + 4] = smid() | (unsigned long long)c.q << 16 |
                              (unsigned long long)c.rows << 32 | (unsigned long long)c.m << 48;
       }
       const uint32_t bbytes = 2u * kBK * 2;  // per token row of the pair
-      const uint32_t bytes_pair = 2u * kATileBytes + bbytes * c.half;
+      const uint32_t bytes_pair = 2u * kATileBytes + bbytes * b_boxes(c.half).rows;
       const int rowq = (c.q - p.q_begin) * p.m_per_q;
       const unsigned long long a0 = p.trace ? gtimer() : 0;
       unsigned long long a_acq = 0;
@@ -389,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         if (c.half_hi) {  // wide tile: the next stage carries only the second sub-tile's B
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader && elect_one()) mbar_expect_tx(&full[stage], bbytes * c.half_hi);
+          if (leader && elect_one()) mbar_expect_tx(&full[stage], bbytes * b_boxes(c.half_hi).rows);
           __syncwarp();
           if (++stage == kStages) {
             stage = 0;
@@ -401,7 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         p.trace[kTW * t + 8] = a_acq;
         p.trace[kTW * t + 9] = gtimer() - a0;
       }
-      t = __shfl_sync(0xffffffffu, t_next, 0);
+      if (leader) rec = tile_locate(p, __shfl_sync(0xffffffffu, t_next, 0), total, lane);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
@@ -414,7 +465,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       while (true) {
         const unsigned long long t_q = p.trace ? gtimer() : 0;
         mbar_wait(&tq_full[slot], tq_phase);
-        const int t = tq[slot];
+        const int4 rec = ld_shared_v4(&tq[slot]);
+        const int t = rec.x;
         __syncwarp();
         if (elect_one()) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
         if (++slot == kTQ) {
@@ -424,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (t >= total) break;
         unsigned long long t_wait = 0;  // trace: time spent waiting for stages
         const unsigned long long t_read = p.trace ? gtimer() : 0;
-        const TileCoord c = tile_coord(p, t);
+        const TileCoord c = coord_of(p, rec);
         const bool wide = c.half_hi != 0;
         const uint32_t idesc = idesc_bf16_m256(2 * c.half);
         const uint32_t idesc_hi = idesc_bf16_m256(wide ? 2 * c.half_hi : 16);
@@ -518,7 +570,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       uint32_t tq_phase = 0;
       while (true) {
         mbar_wait(&tq_full[slot], tq_phase);
-        const int t = tq[slot];
+        const int4 rec = ld_shared_v4(&tq[slot]);
+        const int t = rec.x;
         __syncwarp();
         if (elect_one()) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
         if (++slot == kTQ) {
@@ -526,7 +579,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           tq_phase ^= 1;
         }
         if (t >= total) break;
-        const TileCoord c = tile_coord(p, t);
+        const TileCoord c = coord_of(p, rec);
+        const BBoxes bx0 = b_boxes(c.half), bx1 = b_boxes(c.half_hi ? c.half_hi : 8);
         const unsigned long long b0 = p.trace ? gtimer() : 0;
         unsigned long long b_acq = 0;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -547,15 +601,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             unsigned char *sb = stage_base + stage * kStageBytes + kATileBytes;
             const uint32_t bar = mapa(smem_u32(&full[stage]), 0);
             if (elect_one()) {
-              // half = 8*m rows: one TMA box per set bit of m, largest first (boxes
-              // of 128/64/32/16/8 rows land on 8-row = 1024-B swizzle atoms)
-              int off = 0;
-#pragma unroll 1
-              for (int m8 = half >> 3; m8;) {
-                const int i = 31 - __clz(m8);
-                tma_load_pair(sb + off * 128, &p.tm_b[i], bar, kb * kBK, brow + off, pol_x);
-                off += 8 << i;
-                m8 ^= 1 << i;
+              // boxes of 128/64/32/16/8 rows land on 8-row = 1024-B swizzle atoms
+              const BBoxes bx = sub ? bx1 : bx0;
+              tma_load_pair(sb, &p.tm_b[bx.i0], bar, kb * kBK, brow, pol_x);
+              if (bx.i1 >= 0) {
+                const int off = 8 << bx.i0;
+                tma_load_pair(sb + off * 128, &p.tm_b[bx.i1], bar, kb * kBK, brow + off, pol_x);
               }
             }
             __syncwarp();
@@ -587,7 +638,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t tq_phase = 0;
     while (true) {
       mbar_wait(&tq_full[slot], tq_phase);
-      const int t = tq[slot];
+      const int4 rec = ld_shared_v4(&tq[slot]);
+      const int t = rec.x;
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster_relaxed(mapa(smem_u32(&tq_empty[slot]), 0));
       if (++slot == kTQ) {
@@ -595,7 +647,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         tq_phase ^= 1;
       }
       if (t >= total) break;
-      const TileCoord c = tile_coord(p, t);
+      const TileCoord c = coord_of(p, rec);
       for (int sub = 0; sub < (c.half_hi ? 2 : 1); ++sub, ++use) {
       const int acc = use & 1;
       mbar_wait(&tfull[acc], (use >> 1) & 1);
