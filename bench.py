@@ -455,6 +455,26 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_val = T * args.steps * ws / e2e_s
+    # the same host<->device copies without the layer (3 device buffer sets,
+    # one stream per direction, as janus_moe_layer_host_async issues them): the
+    # host link's ceiling for e2e — the copies of a step outlast its layer
+    h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    xs = [torch.empty_like(x) for _ in range(3)]
+    bs = [torch.empty_like(batches[0]) for _ in range(3)]
+    gs = [torch.empty_like(gw) for _ in range(3)]
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    for i in range(args.steps):
+        k = i % 3
+        with torch.cuda.stream(h2d_s):
+            xs[k].copy_(xh, non_blocking=True)
+            bs[k].copy_(bh[i % N_BATCHES], non_blocking=True)
+            gs[k].copy_(gh, non_blocking=True)
+        with torch.cuda.stream(d2h_s):
+            oh.copy_(xs[(k + 1) % 3], non_blocking=True)
+    torch.cuda.synchronize()
+    copies_s = time.perf_counter() - c0
+    del xs, bs, gs
 
     # scheduler µs/iter (graph-replayed) on the same batch
     sched_us = sched.time_schedule(batches[0], T, K_TOP, reps=51)
@@ -549,7 +569,10 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "tokens/s",
                 "h2d_bytes_per_step": T * D_H * 2 + T * K_TOP * 8,
-                "d2h_bytes_per_step": T * D_H * 2},
+                "d2h_bytes_per_step": T * D_H * 2,
+                "copies_only_value": T * args.steps / copies_s,
+                "copies_only_note": "the same pinned-host copies alone (both directions at "
+                                    "once), no layer: the host link's ceiling for e2e"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
