@@ -850,7 +850,10 @@ def run_box(args):
                                     f"split {A} attention + {M} MoE GPUs; attention->MoE "
                                     f"dispatch and MoE->attention ") +
                                    "combine by " + ("NVSwitch multicast (NVLS) kernels"
-                                                     if box.transport == "nvls"
+                                                     if box.transport == "nvls" else
+                                                     "copy-engine copies (dispatch) and "
+                                                     "peer-memory kernels (combine)"
+                                                     if box.transport == "ce"
                                                      else "peer-memory (P2P) kernels"),
                        "transport": box.transport,
                        "tokens_per_step": T, "tokens_per_moe_gpu": args.tokens,
@@ -926,9 +929,10 @@ def main():
                     help="NVLS combine: partial sums pushed point to point (default) or "
                          "summed by the NVSwitch (multimem.ld_reduce)")
     ap.add_argument("--transport", default="default",
-                    choices=["default", "auto", "p2p", "nvls", "routed"],
+                    choices=["default", "auto", "p2p", "nvls", "routed", "ce"],
                     help="box exchange for --gpus > 1 (auto: NVLS multicast when supported; "
-                         "routed: rows only to the MoE GPUs their slots are scheduled on)")
+                         "routed: rows only to the MoE GPUs their slots are scheduled on; "
+                         "ce: the P2P broadcast moved by the copy engines)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     apply_shape(args.shape)

@@ -277,15 +277,19 @@ janus_status janus_xfer_set_timeout(janus_ctx *ctx, uint64_t timeout_ns);
  * the IPC handle exchange.  Kernels that wait on one another must then still
  * be enqueued in causal order (a rank's wait only after its producers). */
 janus_status janus_xfer_connect_local(janus_ctx *ctx, janus_ctx *const *peers);
-/* Routed transport (0: broadcast, the default; 1: routed), after configure, on
- * every rank.  Routed: each attention rank ships its shard's routing to every
+/* Transport (0: broadcast by SM peer stores, the default; 1: routed; 2:
+ * broadcast by the copy engines), after configure, on every rank.  Copy
+ * engine: the P2P broadcast's rows and routing go by cudaMemcpyAsync into the
+ * MoE ranks' mapped regions and flag_dispatch by a stream memory write after
+ * them — no dispatch kernel, so a colocated rank's MoE kernels keep every SM.
+ * Routed: each attention rank ships its shard's routing to every
  * rank, runs the scheduler over the whole step (identical to the MoE ranks'),
  * and sends each row only to the MoE ranks its slots were scheduled on
  * (north_star's per-GPU buffers; StepTraffic, comm.hpp:20-39); each MoE rank
  * pushes partial sums only for the tokens it computed.  Needs the replica map
  * on the attention ranks' contexts too (janus_set_replica_map), routing shipped
  * (no MoE-side gating) and no shared expert; point to point only (no NVLS). */
-janus_status janus_xfer_set_transport(janus_ctx *ctx, int routed);
+janus_status janus_xfer_set_transport(janus_ctx *ctx, int transport);
 /* NVLS multicast transport (optional, after janus_xfer_connect on every rank):
  * rows, routing and partial sums then move through one NVSwitch multicast
  * object — dispatch leaves an attention GPU once instead of once per MoE GPU,

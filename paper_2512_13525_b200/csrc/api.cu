@@ -845,6 +845,9 @@ static void xfer_release(janus_ctx *ctx) {
     free_assign(x.lay[i]);
     dfree(x.lay_tile[i]);
   }
+  for (cudaStream_t st : x.ce_streams) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : x.ce_done) cudaEventDestroy(ev);
+  if (x.ce_fork) cudaEventDestroy(x.ce_fork);
   x = janus::XferState{};
   ctx->xfer_ready = false;
 }
@@ -891,10 +894,27 @@ janus_status janus_xfer_configure_colocated(janus_ctx *ctx, int n, int rank, int
   return xfer_setup(ctx, n, n, rank, max_tokens, d_h, k, true);
 }
 
-janus_status janus_xfer_set_transport(janus_ctx *ctx, int routed) {
+janus_status janus_xfer_set_transport(janus_ctx *ctx, int transport) {
   if (!ctx || !ctx->xfer.local) return fail(ctx, JANUS_ESTATE, "xfer: configure first");
-  if (routed != 0 && routed != 1) return fail(ctx, JANUS_EINVAL, "xfer: transport must be 0 or 1");
+  if (transport < 0 || transport > 2)
+    return fail(ctx, JANUS_EINVAL, "xfer: transport must be 0 (P2P), 1 (routed) or 2 (copy engine)");
   janus::XferState &x = ctx->xfer;
+  if (transport == janus::kXferCE) {
+    if (x.mc) return fail(ctx, JANUS_EINVAL, "xfer: the copy-engine transport is point to point (no NVLS)");
+    CK(cudaSetDevice(ctx->device));
+    if (x.ce_streams.empty() && x.rank < x.A) {
+      x.ce_streams.resize(x.M);
+      x.ce_done.resize(x.M);
+      for (int g = 0; g < x.M; ++g) {
+        CK(cudaStreamCreateWithFlags(&x.ce_streams[g], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&x.ce_done[g], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&x.ce_fork, cudaEventDisableTiming));
+    }
+    x.transport = janus::kXferCE;
+    return JANUS_OK;
+  }
+  const bool routed = transport == janus::kXferRouted;
   if (routed && x.mc)
     return fail(ctx, JANUS_EINVAL, "xfer: the routed transport is point to point (no NVLS)");
   if (routed && x.M > 32)
@@ -1012,6 +1032,11 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
   if (!d_experts != !d_gate_w)
     return fail(ctx, JANUS_EINVAL, "xfer: pass both routing arrays, or neither (MoE-side gating)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (x.transport == janus::kXferCE) {  // copy engines: no kernel
+    cudaError_t e = janus::launch_dispatch_ce(x, d_x, d_experts, d_gate_w, T, epoch, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "copy-engine dispatch");
+    return JANUS_OK;
+  }
   if (x.transport != janus::kXferRouted) {
     cudaError_t e = janus::launch_dispatch(x, d_x, d_experts, d_gate_w, T, epoch, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "dispatch_kernel");

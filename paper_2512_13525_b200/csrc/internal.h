@@ -153,7 +153,11 @@ struct XferLayout {
 };
 XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k);
 
-enum XferTransport { kXferP2P = 0, kXferRouted = 1 };  // NVLS: XferState::mc
+// NVLS: XferState::mc.  kXferCE: the P2P broadcast's rows moved by the copy
+// engines (cudaMemcpyAsync into the peers' mapped regions, the flag by a
+// stream memory write after them), so the dispatch takes no SM time from the
+// MoE role's kernels running on the same GPU (colocated boxes).
+enum XferTransport { kXferP2P = 0, kXferRouted = 1, kXferCE = 2 };
 
 // Device error words of one rank's exchange endpoint (x.err, int[8]).
 enum XferErr {
@@ -202,6 +206,12 @@ struct XferState {
   unsigned long long mc_va = 0, uc_va = 0;           // multicast / own-backing mappings
   size_t mc_bytes = 0, mc_gran = 0;
   size_t mx_off = 0, mex_off = 0, mgw_off = 0, mpart_off = 0, mslot = 0;  // slot 0; slot 1 = + mslot
+  // copy-engine transport: one stream per MoE rank (the copies to different
+  // ranks run on different engines at once), forked from / joined into the
+  // caller's stream
+  std::vector<cudaStream_t> ce_streams;
+  std::vector<cudaEvent_t> ce_done;
+  cudaEvent_t ce_fork = nullptr;
 };
 constexpr int kCounterKinds = 2;  // 0: row dispatch, 1: routing push
 
@@ -217,6 +227,12 @@ inline size_t xfer_slot(unsigned long long epoch) { return (size_t)(epoch & 1); 
 cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *d_ex,
                             const float *d_gw, long long T, unsigned long long epoch,
                             cudaStream_t s);
+// Copy-engine broadcast (kXferCE), attention rank: the shard rows (+ routing)
+// into every MoE rank's region by cudaMemcpyAsync, then flag_dispatch by
+// cuStreamWriteValue64 (ordered after the copies, with a memory barrier).
+cudaError_t launch_dispatch_ce(const XferState &x, const void *d_x, const int32_t *d_ex,
+                               const float *d_gw, long long T, unsigned long long epoch,
+                               cudaStream_t s);
 // Routed transport, attention rank: shard routing into every rank; flag_route.
 cudaError_t launch_route_push(const XferState &x, const int32_t *d_ex, const float *d_gw,
                               long long T, unsigned long long epoch, cudaStream_t s);

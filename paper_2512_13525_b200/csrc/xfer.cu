@@ -429,6 +429,71 @@ cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *
   return cudaGetLastError();
 }
 
+namespace {
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WriteValue64Fn write_value64_fn() {
+  static WriteValue64Fn fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue64Fn>(ptr);
+  }
+  return fn;
+}
+}  // namespace
+
+cudaError_t launch_dispatch_ce(const XferState &x, const void *d_x, const int32_t *d_ex,
+                               const float *d_gw, long long T, unsigned long long epoch,
+                               cudaStream_t s) {
+  WriteValue64Fn wv = write_value64_fn();
+  if (!wv) return cudaErrorNotSupported;
+  long long first = 0, Ta = 0;
+  shard_host(x, T, first, Ta);
+  const size_t so = xfer_slot(epoch) * x.L.slot_stride;
+  const size_t row = (size_t)x.d_h * 2;
+  const bool fork = (int)x.ce_streams.size() == x.M && x.M > 1;
+  if (fork) {
+    cudaError_t e = cudaEventRecord(x.ce_fork, s);
+    if (e != cudaSuccess) return e;
+  }
+  for (int g = 0; g < x.M; ++g) {
+    unsigned char *base = static_cast<unsigned char *>(x.peer_base[x.moe0 + g]);
+    cudaError_t e = cudaSuccess;
+    cudaStream_t sg = s;
+    if (fork) {  // rank g's copies on their own stream (their own copy engine)
+      sg = x.ce_streams[g];
+      e = cudaStreamWaitEvent(sg, x.ce_fork, 0);
+      if (e != cudaSuccess) return e;
+    }
+    if (Ta > 0) {
+      e = cudaMemcpyAsync(base + x.L.x_off + so + (size_t)first * row, d_x, (size_t)Ta * row,
+                          cudaMemcpyDeviceToDevice, sg);
+      if (e == cudaSuccess && d_ex)
+        e = cudaMemcpyAsync(base + x.L.ex_off + so + (size_t)first * x.k * 4, d_ex,
+                            (size_t)Ta * x.k * 4, cudaMemcpyDeviceToDevice, sg);
+      if (e == cudaSuccess && d_gw)
+        e = cudaMemcpyAsync(base + x.L.gw_off + so + (size_t)first * x.k * 4, d_gw,
+                            (size_t)Ta * x.k * 4, cudaMemcpyDeviceToDevice, sg);
+    }
+    if (e != cudaSuccess) return e;
+    // flag_dispatch[a] = epoch on MoE rank g, after this stream's copies above
+    // (default flags: the write is preceded by a memory barrier)
+    const CUdeviceptr flag =
+        reinterpret_cast<CUdeviceptr>(base + x.L.flag_dispatch_off + 8 * (size_t)x.rank);
+    if (wv(reinterpret_cast<CUstream>(sg), flag, (cuuint64_t)epoch, 0) != CUDA_SUCCESS)
+      return cudaErrorLaunchFailure;
+    if (fork) {
+      e = cudaEventRecord(x.ce_done[g], sg);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, x.ce_done[g], 0);  // join
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_route_push(const XferState &x, const int32_t *d_ex, const float *d_gw,
                               long long T, unsigned long long epoch, cudaStream_t s) {
   long long first = 0, Ta = 0;

@@ -111,7 +111,7 @@ class _Ctx:
             pass
 
 
-TRANSPORTS = ("auto", "p2p", "nvls", "routed")
+TRANSPORTS = ("auto", "p2p", "nvls", "routed", "ce")
 
 
 class JanusBox:
@@ -120,7 +120,9 @@ class JanusBox:
     For an MoE rank pass ``layer`` (a :class:`paper_2512_13525_b200.moe.MoELayer`
     built with ``instance = rank - n_attn`` and its weight store set).
     ``transport``: ``p2p`` / ``nvls`` broadcast every token to every MoE rank
-    (the reference's semantics, comm.hpp:12-14); ``routed`` sends a row only to
+    (the reference's semantics, comm.hpp:12-14) by SM stores; ``ce`` is the P2P
+    broadcast moved by the copy engines (no dispatch kernel: a colocated rank's
+    MoE kernels keep every SM); ``routed`` sends a row only to
     the MoE ranks its slots are scheduled on — attention ranks then also need
     the replica map (``rmap``) to run the scheduler; ``auto`` = NVLS when every
     rank supports it, else P2P.  ``combine`` (NVLS only): ``push`` (default) —
@@ -161,9 +163,9 @@ class JanusBox:
         else:
             self._check(lib.janus_xfer_configure(self._ctx, plan.n_attn, plan.n_moe, rank,
                                                  max_tokens, d_hidden, top_k))
-        self.transport = "routed" if transport == "routed" else "p2p"
-        if transport == "routed":
-            self._check(lib.janus_xfer_set_transport(self._ctx, 1))
+        self.transport = transport if transport in ("routed", "ce") else "p2p"
+        if transport in ("routed", "ce"):
+            self._check(lib.janus_xfer_set_transport(self._ctx, 1 if transport == "routed" else 2))
         if not _connect:
             return
         import torch.distributed as dist
@@ -191,12 +193,12 @@ class JanusBox:
               devices=None, transport: str = "p2p", rmap=None) -> list:
         """Every rank's endpoint in this process (``layers``: rank -> MoELayer
         of the MoE ranks; ``devices``: rank -> device, default 0), connected
-        with raw pointers (janus_xfer_connect_local).  P2P or routed transport.
+        with raw pointers (janus_xfer_connect_local).  P2P, routed or copy-engine transport.
         Calls into ranks that wait on one another must be enqueued in causal
         order (e.g. on one stream: every dispatch, then every MoE step, then
         every combine)."""
-        if transport not in ("p2p", "routed"):
-            raise ValueError("a same-process box uses the p2p or routed transport")
+        if transport not in ("p2p", "routed", "ce"):
+            raise ValueError("a same-process box uses the p2p, routed or ce transport")
         devices = devices or {}
         boxes = [cls(plan, r, max_tokens, d_hidden, top_k, layer=layers.get(r),
                      device=devices.get(r, 0), transport=transport, rmap=rmap, _connect=False)

@@ -38,7 +38,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=300)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out")
-    ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls", "routed"])
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nvls", "routed", "ce"])
     ap.add_argument("--combine", default="push", choices=["push", "switch"])
     ap.add_argument("--shared", action="store_true", help="add a shared expert (NVLS only)")
     ap.add_argument("--shared-split", action="store_true",

@@ -156,7 +156,7 @@ def check_outputs(oracle, weights_of, plan, steps, outs, what):
 CASES = [(1, 1, False), (1, 3, False), (2, 2, False), (2, 2, True), (4, 4, True)]
 
 
-@pytest.mark.parametrize("transport", ["p2p", "routed"])
+@pytest.mark.parametrize("transport", ["p2p", "routed", "ce"])
 @pytest.mark.parametrize("inflight", [1, 2])
 @pytest.mark.parametrize("attn,moe,colocated", CASES)
 def test_box_exchange_vs_oracle(env, oracle, attn, moe, colocated, inflight, transport):
@@ -182,7 +182,7 @@ def test_box_exchange_vs_oracle(env, oracle, attn, moe, colocated, inflight, tra
             "vs_fp32": max(s["vs_fp32"] for s in stats)}}) + "\n")
 
 
-@pytest.mark.parametrize("transport", ["p2p", "routed"])
+@pytest.mark.parametrize("transport", ["p2p", "routed", "ce"])
 def test_unknown_expert_on_moe_rank_raises_on_attention_rank(env, oracle, transport):
     """An unknown expert in one step: every MoE rank's K1 rejects it and
     publishes the status with its combine flag; the attention ranks raise the

@@ -19,7 +19,7 @@ def gpus():
 
 
 @pytest.mark.parametrize("transport,inflight", [("p2p", 1), ("p2p", 2), ("nvls", 1), ("nvls", 2),
-                                               ("routed", 1), ("routed", 2)])
+                                               ("routed", 1), ("routed", 2), ("ce", 1), ("ce", 2)])
 @pytest.mark.parametrize("attn,moe", [(1, 1), (1, 3), (2, 2)])
 def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
     if gpus() < attn + moe:
@@ -27,7 +27,7 @@ def test_box_exchange_matches_single_gpu_layer(attn, moe, transport, inflight):
     out = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={attn + moe}", "--master-addr", "127.0.0.1", "--master-port",
-           str(29500 + 10 * attn + moe + {"p2p": 0, "nvls": 50, "routed": 300}[transport] +
+           str(29500 + 10 * attn + moe + {"p2p": 0, "nvls": 50, "routed": 300, "ce": 400}[transport] +
                100 * inflight),
            os.path.join(ROOT, "tests", "dist_worker.py"),
            "--attn", str(attn), "--moe", str(moe), "--out", out, "--transport", transport,
@@ -96,7 +96,8 @@ def test_box_exchange_shared_expert_and_moe_side_gating(flag):
                 assert s_["bad"] == 0, s_
 
 
-@pytest.mark.parametrize("n,transport", [(2, "nvls"), (4, "nvls"), (4, "p2p"), (4, "routed")])
+@pytest.mark.parametrize("n,transport", [(2, "nvls"), (4, "nvls"), (4, "p2p"), (4, "routed"),
+                                         (2, "ce"), (4, "ce")])
 def test_moe_only_colocated_box(n, transport):
     """The MoE-only box (every rank owns a shard and is an MoE instance), two
     steps in flight."""
@@ -105,7 +106,7 @@ def test_moe_only_colocated_box(n, transport):
     out = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
-           str(29800 + 10 * n + {"nvls": 0, "p2p": 1, "routed": 2}[transport]),
+           str(29800 + 10 * n + {"nvls": 0, "p2p": 1, "routed": 2, "ce": 3}[transport]),
            os.path.join(ROOT, "tests", "dist_worker.py"),
            "--attn", str(n), "--moe", str(n), "--out", out, "--transport", transport,
            "--inflight", "2", "--colocated"]
