@@ -653,10 +653,17 @@ __device__ void greedy_pairs(int lane, int W, int N, bool pairs_only, ActMulti a
           uint32_t da, db;
           asm("prmt.b32 %0, %1, %2, %3;" : "=r"(da) : "r"(lo), "r"(hi), "r"(r[u].x));
           asm("prmt.b32 %0, %1, %2, %3;" : "=r"(db) : "r"(lo), "r"(hi), "r"(r[u].x >> 16));
-          const uint32_t keep_a = da <= db ? 0xffffffffu : 0u;
-          lo += r[u].w ^ ((r[u].y ^ r[u].w) & keep_a);  // unconditional uses: no sunk loads
-          hi += bhs[u] ^ ((r[u].z ^ bhs[u]) & keep_a);
-          o[u] = (int)(keep_a & 1u);
+          // both successors formed beside the PRMTs: the chain per expert is
+          // PRMT -> compare -> select (unconditional uses: no sunk loads)
+          uint32_t la, lb, ha, hb;  // (asm: kept apart from the select, not re-associated)
+          asm("add.u32 %0, %1, %2;" : "=r"(la) : "r"(lo), "r"(r[u].y));
+          asm("add.u32 %0, %1, %2;" : "=r"(lb) : "r"(lo), "r"(r[u].w));
+          asm("add.u32 %0, %1, %2;" : "=r"(ha) : "r"(hi), "r"(r[u].z));
+          asm("add.u32 %0, %1, %2;" : "=r"(hb) : "r"(hi), "r"(bhs[u]));
+          const bool ka = da <= db;
+          lo = ka ? la : lb;
+          hi = ka ? ha : hb;
+          o[u] = (int)ka;
         }
         *reinterpret_cast<int4 *>(res + i) = out;
       }
