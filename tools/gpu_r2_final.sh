@@ -14,5 +14,6 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu"
 $CMD > $O/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"aebs|permute_kernel|grouped_gemm|combine_kernel" -c 40 --csv --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"grouped_gemm|permute_kernel|combine_kernel|aebs" -s 5 -c 5 -o $O/full_t4096 -f $CMD > $O/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"grouped_gemm" -s 6 -c 2 -o $O/full_k4 -f python tools/ffn_probe.py > $O/ncu_full.log 2>&1
 echo "ncu rc=$?"
+
