@@ -153,7 +153,10 @@ def check_outputs(oracle, weights_of, plan, steps, outs, what):
     return stats
 
 
-CASES = [(1, 1, False), (1, 3, False), (2, 2, False), (2, 2, True), (4, 4, True)]
+# ... plus the north_star box split 2A+6E (BASELINE c3) and the 8-GPU MoE-only
+# box the 8-GPU bench runs, every rank on this one GPU
+CASES = [(1, 1, False), (1, 3, False), (2, 2, False), (2, 2, True), (4, 4, True), (2, 6, False),
+         (8, 8, True)]
 
 
 @pytest.mark.parametrize("transport", ["p2p", "routed", "ce"])
