@@ -52,6 +52,7 @@ CONFIGS = {
     "c3_m1": dict(kind="zipf", E=128, k=8, N=1, C=128, seed=0x235, s=1.0),
     "c3_m2": dict(kind="zipf", E=128, k=8, N=2, C=80, seed=0x235, s=1.0),
     "c3_m3": dict(kind="zipf", E=128, k=8, N=3, C=54, seed=0x235, s=1.0),
+    "c3_m4": dict(kind="zipf", E=128, k=8, N=4, C=40, seed=0x235, s=1.0),
 }
 
 
