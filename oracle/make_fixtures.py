@@ -53,6 +53,8 @@ CONFIGS = {
     "c3_m2": dict(kind="zipf", E=128, k=8, N=2, C=80, seed=0x235, s=1.0),
     "c3_m3": dict(kind="zipf", E=128, k=8, N=3, C=54, seed=0x235, s=1.0),
     "c3_m4": dict(kind="zipf", E=128, k=8, N=4, C=40, seed=0x235, s=1.0),
+    "c3_m6": dict(kind="zipf", E=128, k=8, N=6, C=27, seed=0x235, s=1.0),  # = c3 (2A+6E)
+    "c3_m8": dict(kind="zipf", E=128, k=8, N=8, C=20, seed=0x235, s=1.0),
 }
 
 
