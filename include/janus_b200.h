@@ -171,6 +171,13 @@ janus_status janus_profile_read(janus_ctx *ctx, double *sched_ms, double *ffn_ms
  * ns has 8 entries. */
 janus_status janus_trace_schedule(janus_ctx *ctx, const int32_t *d_experts, int num_tokens,
                                   int top_k, int64_t *ns);
+/* Debug: the grouped GEMMs' tile timeline.  With JANUS_GEMM_TRACE=1 in the
+ * environment when the layer is configured, every tile stamps %globaltimer
+ * (draw, MMA start, accumulator ready, epilogue done, producer waits, ...) and
+ * CTA 0 its stages; this copies [2 GEMMs][16384 tiles][16] u64 to host and
+ * clears them (tools/gemm_timeline.py reads it).  Returns 0, or 4 when the
+ * trace was not enabled, 3 on a CUDA error. */
+int janus_debug_ffn_trace(unsigned long long *host, int cap_words);
 
 /* ---- MoE-side gating ------------------------------------ */
 /* Janus gates on the MoE side; the reference only consumes

@@ -35,7 +35,7 @@ SYMBOLS = (
     "janus_xfer_configure_colocated", "janus_xfer_check", "janus_xfer_set_timeout",
     "janus_xfer_connect_local", "janus_xfer_set_transport", "janus_attn_route_async",
     "janus_xfer_recv_rows", "janus_xfer_set_combine", "janus_latency_instance",
-    "janus_latency_layer", "janus_latency_fit",
+    "janus_latency_layer", "janus_latency_fit", "janus_debug_ffn_trace",
 )
 
 
@@ -84,6 +84,8 @@ def _load() -> C.CDLL:
     L.janus_profile.argtypes = [vp, i32]
     L.janus_profile_read.argtypes = [vp, P(dbl), P(dbl), P(i32)]
     L.janus_trace_schedule.argtypes = [vp, vp, i32, i32, P(i64)]
+    L.janus_debug_ffn_trace.argtypes = [vp, i32]
+    L.janus_debug_ffn_trace.restype = i32
     L.janus_xfer_configure.argtypes = [vp, i32, i32, i32, i32, i32, i32]
     L.janus_xfer_handle.argtypes = [vp, C.c_char_p]
     L.janus_xfer_connect.argtypes = [vp, C.c_char_p]

@@ -121,8 +121,6 @@ def main():
         layer.forward(x, batches[i % len(batches)], gw, out=out)
     torch.cuda.synchronize()
     fn = lib.janus_debug_ffn_trace
-    fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    fn.restype = ctypes.c_int
     buf = np.zeros(2 * TRACE_TILES * TW, dtype=np.uint64)
     assert fn(buf.ctypes.data, buf.size) == 0  # read + clear the warm-up steps' stamps
     # one more step, after an L2 flush, then read its timeline
