@@ -51,8 +51,17 @@ def main():
                     help="2: dispatch step s+1 before combining step s (double-buffered slots)")
     args = ap.parse_args()
     rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # JANUS_TEST_GPUS=n: more ranks than GPUs (rank r on GPU r % n; the
+    # exchange's protocol at a world the box does not have, e.g. 8 ranks);
+    # torch.distributed then runs on gloo (plumbing only: IPC handles, barriers)
+    ngpu = int(os.environ.get("JANUS_TEST_GPUS", "0"))
+    if ngpu:
+        local = local % ngpu
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     plan = BoxPlan.moe_only(args.moe) if args.colocated else BoxPlan(args.attn, args.moe)
     assert dist.get_world_size() == plan.world
     E, k, d_h, d_e, T = 16, 4, 256, 128, args.tokens

@@ -119,3 +119,28 @@ def test_moe_only_colocated_box(n, transport):
         assert r["role"] == "both"
         for s_ in r["steps"]:
             assert s_["bad"] == 0, s_
+
+
+@pytest.mark.parametrize("transport", ["routed", "ce"])
+def test_moe_only_box_8_ranks_oversubscribed(transport):
+    """The 8-rank MoE-only box (the 8-GPU bench's default) as 8 processes on
+    the GPUs there are (rank r on GPU r % n; CUDA IPC between processes, also
+    on one device): every shard vs the fp32 oracle, two steps in flight."""
+    n = max(1, min(gpus(), 8))
+    out = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port",
+           str(29950 + {"routed": 0, "ce": 1}[transport]),
+           os.path.join(ROOT, "tests", "dist_worker.py"),
+           "--attn", "8", "--moe", "8", "--out", out, "--transport", transport,
+           "--inflight", "2", "--colocated", "--steps", "3", "--tokens", "160"]
+    env = dict(os.environ, JANUS_TEST_GPUS=str(n))
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
+    assert len(res) == 8
+    for r in res:
+        assert not r["timed_out"], r
+        assert r["role"] == "both"
+        for s_ in r["steps"]:
+            assert s_["bad"] == 0, s_
