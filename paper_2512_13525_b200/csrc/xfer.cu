@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -353,6 +354,20 @@ int grid_for(long long work, int per_block = 256) {
   return (int)std::max<long long>(1, std::min<long long>(b, (long long)sms * 8));
 }
 
+// Grid of a dispatch-side exchange kernel, which runs beside this GPU's MoE
+// kernels in the MoE-only box (the next step's rows move while this step's
+// grouped GEMMs run): a third of the SMs.  (The owner's reduce stays on the
+// full grid: it is on the step's critical path — capped, the combine went
+// from 27 to 197 us.)  Its CTAs co-reside with the GEMM's one
+// CTA per SM; on every SM they slowed every tile pair (4-GPU box: 8.2 M ->
+// 8.8 M tok/s/GPU with 40-80 dispatch CTAs instead of the full grid, measured).
+int side_grid(long long work) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::min(grid_for(work), std::max(8, sms / 3));
+}
+
 PeerPtrs peer_ptrs(const XferState &x) {
   PeerPtrs p{};
   for (int r = 0; r < x.world && r < kMaxPeers; ++r)
@@ -423,7 +438,7 @@ cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *
     dst.ex_off = x.L.ex_off + so;
     dst.gw_off = x.L.gw_off + so;
   }
-  dispatch_kernel<<<grid_for(std::max<long long>(Ta * x.d_h / 8, 1)), 256, 0, s>>>(
+  dispatch_kernel<<<side_grid(std::max<long long>(Ta * x.d_h / 8, 1)), 256, 0, s>>>(
       dst, peer_ptrs(x), x.M, x.moe0, x.rank, reinterpret_cast<const uint4 *>(d_x), d_ex, d_gw,
       first, Ta, vec, x.k, x.L, epoch, counter_for(x, 0, epoch));
   return cudaGetLastError();
@@ -499,7 +514,7 @@ cudaError_t launch_route_push(const XferState &x, const int32_t *d_ex, const flo
   long long first = 0, Ta = 0;
   shard_host(x, T, first, Ta);
   const size_t so = xfer_slot(epoch) * x.L.slot_stride;
-  route_push_kernel<<<grid_for(std::max<long long>(Ta * x.k, 1)), 256, 0, s>>>(
+  route_push_kernel<<<side_grid(std::max<long long>(Ta * x.k, 1)), 256, 0, s>>>(
       peer_ptrs(x), x.world, x.rank, d_ex, d_gw, first, Ta * x.k, x.k, x.L.ex_off + so,
       x.L.gw_off + so, x.L, epoch, counter_for(x, 1, epoch));
   return cudaGetLastError();
@@ -511,7 +526,7 @@ cudaError_t launch_routed_dispatch(const XferState &x, const void *d_x, const in
   long long first = 0, Ta = 0;
   shard_host(x, T, first, Ta);
   const size_t so = xfer_slot(epoch) * x.L.slot_stride;
-  routed_dispatch_kernel<<<grid_for(std::max<long long>(Ta * 32, 1)), 256, 0, s>>>(
+  routed_dispatch_kernel<<<side_grid(std::max<long long>(Ta * 32, 1)), 256, 0, s>>>(
       peer_ptrs(x), x.M, x.moe0, x.rank, reinterpret_cast<const uint4 *>(d_x), inst, status,
       first, Ta, x.d_h / 8, x.k, x.L.x_off + so, x.dmask + xfer_slot(epoch) * x.L.ta_max, x.err,
       x.L, epoch, counter_for(x, 0, epoch));

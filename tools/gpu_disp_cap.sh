@@ -1,0 +1,6 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+for cap in ${CAPS:-24 40 48 64 80 96}; do
+  JANUS_DISPATCH_CTAS=$cap timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $((29600 + cap)) bench.py --gpus 4 --steps 50 --warmup 5 --no-cpu > /tmp/b.json 2>/tmp/b.err
+  tail -1 /tmp/b.json | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); n=d['nvlink']; print('cap $cap', 'value %.3fM'%(d['value']/1e6), 'ms %.1f'%(d['ms_per_step']*1e3), 'disp %.1f moe %.1f comb %.1f'%(n['dispatch_us'],n['moe_step_us'],n['combine_us']), 'ffn %.1f'%d['roofline']['ffn_us_per_step'])"
+done
