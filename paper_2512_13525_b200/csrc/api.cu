@@ -159,6 +159,30 @@ void janus_destroy(janus_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  {  // the exchange's own streams (partial-sum push, copy-engine dispatch)
+    janus::XferState &x = ctx->xfer;
+    if (x.push_stream) {
+      cudaStreamSynchronize(x.push_stream);
+      cudaStreamDestroy(x.push_stream);
+      x.push_stream = nullptr;
+    }
+    for (int i = 0; i < 2; ++i) {
+      if (x.ffn_done[i]) cudaEventDestroy(x.ffn_done[i]);
+      if (x.push_done[i]) cudaEventDestroy(x.push_done[i]);
+      if (x.own_disp[i]) cudaEventDestroy(x.own_disp[i]);
+      if (x.own_sig[i]) cudaEventDestroy(x.own_sig[i]);
+      x.ffn_done[i] = x.push_done[i] = x.own_disp[i] = x.own_sig[i] = nullptr;
+    }
+    for (cudaStream_t st : x.ce_streams) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+    x.ce_streams.clear();
+    for (cudaEvent_t ev : x.ce_done) cudaEventDestroy(ev);
+    x.ce_done.clear();
+    if (x.ce_fork) cudaEventDestroy(x.ce_fork);
+    x.ce_fork = nullptr;
+  }
   free_map(ctx->dmap);
   dfree(ctx->d_in);
   free_assign(ctx->d_out);
@@ -167,6 +191,7 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->ffn.xp);
   dfree(ctx->ffn.h);
   dfree(ctx->ffn.y);
+  dfree(ctx->ffn.y2);
   dfree(ctx->ffn.tile_ctr);
   dfree(ctx->d_x);
   dfree(ctx->d_outbuf);
@@ -522,6 +547,8 @@ janus_status janus_moe_configure(janus_ctx *ctx, int d_h, int d_e, int max_token
   dfree(ctx->ffn.xp);
   dfree(ctx->ffn.h);
   dfree(ctx->ffn.y);
+  dfree(ctx->ffn.y2);
+  ctx->ffn.y2 = nullptr;
   dfree(ctx->ffn.tile_ctr);
   ctx->ffn.tile_ctr = nullptr;
   free_host_pipe(ctx);  // staging sized by max_tokens
@@ -657,6 +684,17 @@ static int layer_tile_n(const janus_ctx *ctx, int T) {
 
 // pre / pre_tile (optional): this step's layout, computed earlier by the same
 // context's attention role (colocated routed box) — K1 is then not rerun.
+// Blocks (4 warps each) of the side-stream partial-sum push: enough warps in
+// flight for its gather latency without flooding the SMs beside the next
+// step's GEMMs.  Measured (4-GPU box, tok/s/GPU): 1 x SMs 7.1 M, 2 x 8.9 M,
+// 3 x 9.4 M, 4 x 9.7-9.8 M, 5 x 9.6 M, 6 x 9.3 M, uncapped 9.1 M.
+static int push_blocks() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return 4 * sms;
+}
+
 static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,
                               const float *d_gate_w, int T, void *d_out,
                               const janus_assignment *assign, cudaStream_t s,
@@ -743,7 +781,16 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
   if (e != cudaSuccess) return cuda_fail(ctx, e, "permute_kernel");
   int launches = 0;
   if (ev) CK(cudaEventRecord(ev[2], s));
-  e = janus::launch_ffn(p, a.group_off, tile_off, s, &launches);
+  // the colocated routed MoE role pushes its partial sums on a side stream
+  // over y[epoch slot], beside the next step's permute and GEMMs (measured:
+  // the push is ~85 us of a 4-GPU step); the GEMMs that write y[slot] again
+  // two steps later wait for that push
+  const janus::XferState &xs = ctx->xfer;
+  const int psl = (int)janus::xfer_slot(push_epoch);
+  const bool side_push = push_epoch && pre && !shared && !xs.mc && xs.push_stream && p.y2 &&
+                         xs.transport == janus::kXferRouted && !xs.local_connect;
+  if (side_push) CK(cudaStreamWaitEvent(s, xs.push_done[psl], 0));
+  e = janus::launch_ffn(p, a.group_off, tile_off, s, &launches, side_push ? psl : 0);
   if (e == cudaSuccess && shared)
     e = janus::launch_ffn(ps, ctx->shared_off, ctx->shared_off + 2, s, &launches);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "grouped_gemm_kernel");
@@ -765,10 +812,26 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
         return fail(ctx, JANUS_EUNSUPPORTED,
                     "moe: the shared expert needs a broadcast transport (P2P or NVLS)");
       const janus::PushDst pd = janus::push_dst(x, push_epoch);
+      if (side_push) {
+        CK(cudaEventRecord(x.ffn_done[psl], s));
+        CK(cudaStreamWaitEvent(x.push_stream, x.ffn_done[psl], 0));
+        e = janus::launch_combine(psl ? p.y2 : p.y, a.slot_row, a.instance, ctx->instance,
+                                  d_gate_w, T, k, p.d_h, nullptr, x.push_stream, nullptr, 0, 0,
+                                  a.status, &pd, push_blocks());
+        if (e == cudaSuccess) e = janus::launch_signal_combine(x, a.status, push_epoch, x.push_stream);
+        if (e == cudaSuccess) e = cudaEventRecord(x.push_done[psl], x.push_stream);
+        if (e == cudaSuccess && x.own_sig[psl]) e = cudaEventRecord(x.own_sig[psl], x.push_stream);
+        launches += 1;
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
+        ctx->launches += 2 + launches;
+        return JANUS_OK;
+      }
       e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
                                 nullptr, s, shared ? ps.y : nullptr, sh0, sh1, a.status, &pd);
     }
     if (e == cudaSuccess) e = janus::launch_signal_combine(x, a.status, push_epoch, s);
+    if (e == cudaSuccess && x.own_sig[janus::xfer_slot(push_epoch)])
+      e = cudaEventRecord(x.own_sig[janus::xfer_slot(push_epoch)], s);
     launches += 1;
   } else
     e = janus::launch_combine(p.y, a.slot_row, a.instance, ctx->instance, d_gate_w, T, k, p.d_h,
@@ -845,6 +908,16 @@ static void xfer_release(janus_ctx *ctx) {
     free_assign(x.lay[i]);
     dfree(x.lay_tile[i]);
   }
+  if (x.push_stream) {
+    cudaStreamSynchronize(x.push_stream);
+    cudaStreamDestroy(x.push_stream);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (x.ffn_done[i]) cudaEventDestroy(x.ffn_done[i]);
+    if (x.push_done[i]) cudaEventDestroy(x.push_done[i]);
+    if (x.own_disp[i]) cudaEventDestroy(x.own_disp[i]);
+    if (x.own_sig[i]) cudaEventDestroy(x.own_sig[i]);
+  }
   for (cudaStream_t st : x.ce_streams) cudaStreamDestroy(st);
   for (cudaEvent_t ev : x.ce_done) cudaEventDestroy(ev);
   if (x.ce_fork) cudaEventDestroy(x.ce_fork);
@@ -881,6 +954,11 @@ static janus_status xfer_setup(janus_ctx *ctx, int n_attn, int n_moe, int rank, 
   CK(cudaMemset(x.err, 0, sizeof(int) * janus::kErrWords));
   x.peer_base.assign(x.world, nullptr);
   x.peer_base[rank] = x.local;
+  if (colocated)
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&x.own_disp[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&x.own_sig[i], cudaEventDisableTiming));
+    }
   return JANUS_OK;
 }
 
@@ -933,6 +1011,17 @@ janus_status janus_xfer_set_transport(janus_ctx *ctx, int transport) {
                         JANUS_MAX_EXPERTS, JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
         CK(dalloc(&x.lay_tile[i], JANUS_MAX_REPLICAS + 1));
         CK(cudaMemset(x.lay_tile[i], 0, sizeof(int32_t) * (JANUS_MAX_REPLICAS + 1)));
+      }
+      // the MoE role's partial-sum push on its own stream over a second y
+      janus::FfnPlan &p = ctx->ffn;
+      if (!p.y2) {
+        CK(cudaMalloc(&p.y2, (size_t)p.S_alloc * p.d_h * 2));
+        if (p.w13) CK(janus::build_ffn_tensor_maps(p));  // with y2's map
+      }
+      CK(cudaStreamCreateWithFlags(&x.push_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&x.ffn_done[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&x.push_done[i], cudaEventDisableTiming));
       }
     }
   }
@@ -1000,6 +1089,7 @@ janus_status janus_xfer_connect_local(janus_ctx *ctx, janus_ctx *const *peers) {
     }
     x.peer_base[r] = p->xfer.local;
   }
+  x.local_connect = true;
   ctx->xfer_ready = true;
   return JANUS_OK;
 }
@@ -1032,13 +1122,17 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
   if (!d_experts != !d_gate_w)
     return fail(ctx, JANUS_EINVAL, "xfer: pass both routing arrays, or neither (MoE-side gating)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // a colocated rank's MoE role waits for this dispatch by an event
+  const cudaEvent_t own = x.own_disp[janus::xfer_slot(epoch)];
   if (x.transport == janus::kXferCE) {  // copy engines: no kernel
     cudaError_t e = janus::launch_dispatch_ce(x, d_x, d_experts, d_gate_w, T, epoch, s);
+    if (e == cudaSuccess && own) e = cudaEventRecord(own, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "copy-engine dispatch");
     return JANUS_OK;
   }
   if (x.transport != janus::kXferRouted) {
     cudaError_t e = janus::launch_dispatch(x, d_x, d_experts, d_gate_w, T, epoch, s);
+    if (e == cudaSuccess && own) e = cudaEventRecord(own, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "dispatch_kernel");
     ctx->launches += 1;
     return JANUS_OK;
@@ -1077,6 +1171,7 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
                                  abort_flag);
   if (st != JANUS_OK) return st;
   e = janus::launch_routed_dispatch(x, d_x, ra.instance, ra.status, T, epoch, s);
+  if (e == cudaSuccess && own) e = cudaEventRecord(own, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "routed_dispatch_kernel");
   ctx->launches += 1;
   return JANUS_OK;
@@ -1092,7 +1187,11 @@ janus_status janus_moe_layer_xfer_async(janus_ctx *ctx, int64_t T, uint64_t epoc
   if (ctx->router && x.transport == janus::kXferRouted)
     return fail(ctx, JANUS_EINVAL, "xfer: MoE-side gating needs a broadcast transport");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = janus::launch_wait(x, 0, epoch, s);
+  // own attention role (colocated): ordered by its event, not spun on (the
+  // host enqueues a step's dispatch before its MoE step)
+  const cudaEvent_t own = x.own_disp[janus::xfer_slot(epoch)];
+  if (own) CK(cudaStreamWaitEvent(s, own, 0));
+  cudaError_t e = janus::launch_wait(x, 0, epoch, s, own ? x.rank : -1);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
   ctx->launches += 1;
   const int *abort_flag = x.err + janus::kErrSkip + 0;  // a shard never arrived
@@ -1137,7 +1236,11 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, ui
   int64_t first = 0, Ta = 0;
   janus_shard_tokens(T, x.A, x.rank, &first, &Ta);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = janus::launch_wait(x, 1, epoch, s);
+  // own MoE role (colocated): ordered by its event (the host enqueues a
+  // step's MoE step before its combine), not spun on
+  const cudaEvent_t own = x.own_sig[janus::xfer_slot(epoch)];
+  if (own) CK(cudaStreamWaitEvent(s, own, 0));
+  cudaError_t e = janus::launch_wait(x, 1, epoch, s, own ? x.rank - x.moe0 : -1);
   if (e == cudaSuccess)
     e = x.mc && x.mc_reduce ? janus::launch_reduce_mc(x, d_out, first, Ta, epoch, s)
                             : janus::launch_reduce_partials(x, d_out, Ta, epoch, s);

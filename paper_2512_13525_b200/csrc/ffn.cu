@@ -112,19 +112,17 @@ __device__ __forceinline__ void shard_of(long long T, int A, long long t, int &a
 // Push mode (push.A > 0, the box exchange): the partial sum of token t goes
 // straight into its owning attention rank's region over NVLink (the combine
 // fused with the transfer); skip_empty drops tokens with no slot here.
+// One warp task: one 32 * kCombU-chunk segment of token t's output row.
 template <int G>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
-    combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
-                   const int32_t *__restrict__ slot_inst, int instance,
-                   const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out,
-                   const uint4 *__restrict__ y_shared, int sh0, int sh1,
-                   const int32_t *__restrict__ status, const PushDst push) {
-  sm100::pdl_trigger();
-  sm100::pdl_wait();  // y from the down GEMM
-  const int lane = threadIdx.x & 31;
-  const int segs = (vec + 32 * kCombU - 1) / (32 * kCombU);
-  const int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (task >= T * segs) return;
+__device__ __forceinline__ void combine_task(int task, int segs, int lane,
+                                             const uint4 *__restrict__ y,
+                                             const int32_t *__restrict__ slot_row,
+                                             const int32_t *__restrict__ slot_inst, int instance,
+                                             const float *__restrict__ gw, int T, int k, int vec,
+                                             uint4 *__restrict__ out,
+                                             const uint4 *__restrict__ y_shared, int sh0, int sh1,
+                                             const int32_t *__restrict__ status,
+                                             const PushDst &push) {
   const int t = task / segs, c0 = (task % segs) * 32 * kCombU + lane;
   uint4 *orow = out + (size_t)t * vec;
   if (push.A > 0) {
@@ -232,6 +230,24 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
   }
 }
 
+template <int G>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4)
+    combine_kernel(const uint4 *__restrict__ y, const int32_t *__restrict__ slot_row,
+                   const int32_t *__restrict__ slot_inst, int instance,
+                   const float *__restrict__ gw, int T, int k, int vec, uint4 *__restrict__ out,
+                   const uint4 *__restrict__ y_shared, int sh0, int sh1,
+                   const int32_t *__restrict__ status, const PushDst push) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();  // y from the down GEMM
+  const int lane = threadIdx.x & 31;
+  const int segs = (vec + 32 * kCombU - 1) / (32 * kCombU);
+  const int stride = gridDim.x * kWarpsPerBlock;  // a capped grid (push beside the next GEMMs)
+  for (int task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); task < T * segs;
+       task += stride)
+    combine_task<G>(task, segs, lane, y, slot_row, slot_inst, instance, gw, T, k, vec, out,
+                    y_shared, sh0, sh1, status, push);
+}
+
 }  // namespace
 
 cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t *slot_instance,
@@ -250,11 +266,12 @@ cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t
 cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t *slot_instance,
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
                            cudaStream_t s, const void *y_shared, int sh0, int sh1,
-                           const int32_t *status, const PushDst *push) {
+                           const int32_t *status, const PushDst *push, int max_blocks) {
   if (T == 0) return cudaSuccess;
   const int vec = d_h / 8;
   const int tasks = T * ((vec + 32 * kCombU - 1) / (32 * kCombU));
-  const int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (max_blocks > 0) blocks = std::min(blocks, max_blocks);
   PushDst pd{};
   if (push) pd = *push;
   return sm100::launch_pdl(combine_kernel<4>, dim3(blocks), dim3(32 * kWarpsPerBlock), 0, s,

@@ -816,7 +816,8 @@ cudaError_t build_ffn_tensor_maps(FfnPlan &p) {
   }
   if (ok) {
     ok = make_out_map(&p.tm_h_out, p.h, p.S_alloc, p.d_e, 16) &&
-         make_out_map(&p.tm_y_out, p.y, p.S_alloc, p.d_h, 32);
+         make_out_map(&p.tm_y_out, p.y, p.S_alloc, p.d_h, 32) &&
+         (!p.y2 || make_out_map(&p.tm_y_out2, p.y2, p.S_alloc, p.d_h, 32));
   }
   p.maps_ready = ok;
   return ok ? cudaSuccess : cudaErrorInvalidValue;
@@ -844,7 +845,7 @@ cudaError_t launch_gemm(const GemmParams &g, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
-                       cudaStream_t s, int *launches) {
+                       cudaStream_t s, int *launches, int ybuf) {
   GemmParams g{};
   g.trace = g_trace;
   g.group_off = group_off;
@@ -871,13 +872,14 @@ cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t
   // down: y = h Wd^T, 256 output features per tile
   g.tm_a = p.tm_w2;
   for (int i = 0; i < 5; ++i) g.tm_b[i] = p.tm_h[i];
-  g.tm_out = p.tm_y_out;
+  const bool alt = ybuf && p.y2;
+  g.tm_out = alt ? p.tm_y_out2 : p.tm_y_out;
   g.ctr = p.tile_ctr + 2;
   g.K = p.d_e;
   g.m_tiles = p.d_h / 256;
   g.m_per_q = p.d_h;
   g.up_off = 0;
-  g.out = reinterpret_cast<__nv_bfloat16 *>(p.y);
+  g.out = reinterpret_cast<__nv_bfloat16 *>(alt ? p.y2 : p.y);
   g.out_ld = p.d_h;
   if (g.trace) g.trace += (size_t)kTraceTiles * kTW;
   err = decode ? launch_gemm<kPlain, 32>(g, s) : launch_gemm<kPlain, 128>(g, s);

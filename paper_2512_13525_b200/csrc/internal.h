@@ -87,6 +87,11 @@ struct FfnPlan {
   CUtensorMap tm_w13, tm_w2;
   CUtensorMap tm_xp[5], tm_h[5];  // box rows 8/16/32/64/128 (half of a pair's N)
   CUtensorMap tm_h_out, tm_y_out;  // epilogue TMA stores (box 16 / 32 features x 32 rows)
+  // a second y for the box's MoE role (colocated routed ranks): step s's
+  // partial-sum push reads y[s & 1] on a side stream while step s+1's GEMMs
+  // write the other one
+  void *y2 = nullptr;
+  CUtensorMap tm_y_out2;
   bool maps_ready = false;
 };
 
@@ -99,7 +104,7 @@ cudaError_t launch_permute(const void *x, const int32_t *slot_row, const int32_t
                            cudaStream_t s, const int32_t *status = nullptr);
 // gate/up GEMM with fused SwiGLU, then the down GEMM; 2 launches.
 cudaError_t launch_ffn(const FfnPlan &p, const int32_t *group_off, const int32_t *tile_off,
-                       cudaStream_t s, int *launches);
+                       cudaStream_t s, int *launches, int ybuf = 0);
 // K5 push mode (box exchange): token t's partial sum goes to its owning
 // attention rank a (shard rule, comm.cpp:76-81) at part[g][t - first_a] of that
 // rank's region; skip_empty: tokens with no slot on this instance send nothing.
@@ -117,7 +122,7 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
                            int instance, const float *gate_w, int T, int k, int d_h, void *out,
                            cudaStream_t s, const void *y_shared = nullptr, int sh0 = 0,
                            int sh1 = 0, const int32_t *status = nullptr,
-                           const PushDst *push = nullptr);
+                           const PushDst *push = nullptr, int max_blocks = 0);
 
 // MoE-side gating (gate.cu): router GEMM + top-k + softmax of the top-k logits.
 bool gate_shape_ok(int d_h, int E, int k);
@@ -212,6 +217,17 @@ struct XferState {
   std::vector<cudaStream_t> ce_streams;
   std::vector<cudaEvent_t> ce_done;
   cudaEvent_t ce_fork = nullptr;
+  // colocated routed MoE role: step s's partial-sum push (K5 + signal) runs on
+  // push_stream, beside step s+1's permute and GEMMs (ffn_done / push_done per
+  // epoch slot order it after its GEMMs and the GEMMs two steps later after it)
+  cudaStream_t push_stream = nullptr;
+  cudaEvent_t ffn_done[2] = {nullptr, nullptr}, push_done[2] = {nullptr, nullptr};
+  // a colocated rank's two roles run on different streams of one GPU: the MoE
+  // role orders itself after its own attention role's dispatch, and the
+  // attention role's combine after its own MoE role's signal, by these events
+  // (per epoch slot) — it spins only on the other GPUs' flags
+  cudaEvent_t own_disp[2] = {nullptr, nullptr}, own_sig[2] = {nullptr, nullptr};
+  bool local_connect = false;  // every rank in this process (janus_xfer_connect_local)
 };
 constexpr int kCounterKinds = 2;  // 0: row dispatch, 1: routing push
 
@@ -230,6 +246,8 @@ cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *
 // Copy-engine broadcast (kXferCE), attention rank: the shard rows (+ routing)
 // into every MoE rank's region by cudaMemcpyAsync, then flag_dispatch by
 // cuStreamWriteValue64 (ordered after the copies, with a memory barrier).
+// Grid cap for an exchange kernel that runs beside this GPU's grouped GEMMs.
+int side_grid(long long work);
 cudaError_t launch_dispatch_ce(const XferState &x, const void *d_x, const int32_t *d_ex,
                                const float *d_gw, long long T, unsigned long long epoch,
                                cudaStream_t s);
@@ -244,7 +262,10 @@ cudaError_t launch_routed_dispatch(const XferState &x, const void *d_x, const in
                                    cudaStream_t s);
 // Wait for flags (kind 0 dispatch, 1 combine, 2 route) of `epoch`; the combine
 // wait also collects the MoE ranks' error slots.  Sets err[kErrSkip].
-cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, cudaStream_t s);
+// skip: a flag index not to spin on (a colocated rank's own role: ordered by
+// an event instead — no kernel waits on another of the same GPU by spinning)
+cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, cudaStream_t s,
+                        int skip = -1);
 // MoE rank: publish {status} + flag_combine[g] = epoch on every attention rank,
 // after this rank's partial sums landed (P2P push, or its multicast backing).
 cudaError_t launch_signal_combine(const XferState &x, const int32_t *status,

@@ -223,13 +223,14 @@ __global__ void routed_dispatch_kernel(PeerPtrs peers, int M, int moe0, int a,
 // tells the step's later kernels whether to skip.
 __global__ void wait_flags_kernel(const unsigned long long *flags, int n,
                                   unsigned long long epoch, const int2 *errs, int *err, int kind,
-                                  unsigned long long timeout_ns) {
+                                  unsigned long long timeout_ns, int skip) {
   const int lane = threadIdx.x;
   const unsigned long long t0 = gtimer();
   bool done = false;
   while (!done) {
     bool mine = true;
-    for (int i = lane; i < n; i += 32) mine = mine && ld_acquire_sys(flags + i) >= epoch;
+    for (int i = lane; i < n; i += 32)
+      mine = mine && (i == skip || ld_acquire_sys(flags + i) >= epoch);
     done = __all_sync(0xffffffffu, mine);
     if (!done) {
       if (gtimer() - t0 > timeout_ns) {
@@ -354,20 +355,6 @@ int grid_for(long long work, int per_block = 256) {
   return (int)std::max<long long>(1, std::min<long long>(b, (long long)sms * 8));
 }
 
-// Grid of a dispatch-side exchange kernel, which runs beside this GPU's MoE
-// kernels in the MoE-only box (the next step's rows move while this step's
-// grouped GEMMs run): a third of the SMs.  (The owner's reduce stays on the
-// full grid: it is on the step's critical path — capped, the combine went
-// from 27 to 197 us.)  Its CTAs co-reside with the GEMM's one
-// CTA per SM; on every SM they slowed every tile pair (4-GPU box: 8.2 M ->
-// 8.8 M tok/s/GPU with 40-80 dispatch CTAs instead of the full grid, measured).
-int side_grid(long long work) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return std::min(grid_for(work), std::max(8, sms / 3));
-}
-
 PeerPtrs peer_ptrs(const XferState &x) {
   PeerPtrs p{};
   for (int r = 0; r < x.world && r < kMaxPeers; ++r)
@@ -386,6 +373,21 @@ unsigned *counter_for(const XferState &x, int kind, unsigned long long epoch) {
 }
 
 }  // namespace
+
+// Grid of a dispatch-side exchange kernel, which runs beside this GPU's MoE
+// kernels in the MoE-only box (the next step's rows move while this step's
+// grouped GEMMs run): a third of the SMs.  (The owner's reduce stays on the
+// full grid: it is on the step's critical path — capped, the combine went
+// from 27 to 197 us.)  Its CTAs co-reside with the GEMM's one
+// CTA per SM; on every SM they slowed every tile pair (4-GPU box: 8.2 M ->
+// 8.8 M tok/s/GPU with 40-80 dispatch CTAs instead of the full grid, measured).
+int side_grid(long long work) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::min(grid_for(work), std::max(8, sms / 3));
+}
+
 
 XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
   XferLayout L{};
@@ -533,7 +535,8 @@ cudaError_t launch_routed_dispatch(const XferState &x, const void *d_x, const in
   return cudaGetLastError();
 }
 
-cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, cudaStream_t s) {
+cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, cudaStream_t s,
+                        int skip) {
   unsigned char *base = static_cast<unsigned char *>(x.local);
   const size_t off = kind == 0 ? x.L.flag_dispatch_off
                                : kind == 1 ? x.L.flag_combine_off : x.L.flag_route_off;
@@ -542,7 +545,7 @@ cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, 
       kind == 1 ? reinterpret_cast<const int2 *>(base + x.L.err_off + xfer_slot(epoch) * x.L.slot_stride)
                 : nullptr;
   wait_flags_kernel<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned long long *>(base + off), n,
-                                     epoch, errs, x.err, kind, x.timeout_ns);
+                                     epoch, errs, x.err, kind, x.timeout_ns, skip);
   return cudaGetLastError();
 }
 
