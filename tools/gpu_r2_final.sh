@@ -1,6 +1,6 @@
 #!/bin/bash
 # round 2 end-of-round evidence on one B200: the -m gpu suite, smoke, bench (both arms),
-# the ncu launch list of the bench and one --set full capture of the grouped GEMMs
+# the ncu launch list of the bench (one ncu per call; the --set full captures are tools/gpu_ncu_*.sh)
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 O=gpurun_out/r2final
 mkdir -p $O
@@ -13,7 +13,6 @@ timeout 900 python bench.py --tokens 256 --steps 200 --warmup 10 --no-cpu > $O/b
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu"
 $CMD > $O/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"aebs|permute_kernel|grouped_gemm|combine_kernel" -c 40 --csv --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"grouped_gemm" -s 6 -c 2 -o $O/full_k4 -f python tools/ffn_probe.py > $O/ncu_full.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"aebs|permute_kernel|grouped_gemm|combine_kernel" -c 40 --csv --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1
 echo "ncu rc=$?"
 
