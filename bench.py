@@ -13,9 +13,11 @@ so every step streams it from HBM.
 
 Under torchrun (N > 1) the ranks form one NVLink box (BoxPlan.for_gpus: 1A+1E,
 1A+3E, 2A+6E): attention GPUs dispatch their token shards to the MoE GPUs and
-combine the partial sums.  ``value`` is then the whole box's
-tokens/s divided by ALL N GPUs (per-GPU, as the metric says); the per-MoE-GPU
-figure is a side field.
+combine the partial sums.  ``value`` is the whole job's
+tokens/s over all N GPUs (the contract's aggregate; metric
+"moe_layer_tokens_per_s"); BASELINE's per-GPU figure is the side field
+``tokens_per_s_per_gpu`` (= value / N), the per-MoE-GPU one
+another.
 
 Input generation (routing batches) is test infrastructure — the reference's
 gen_batch through oracle/_ref, or the pinned oracle restatement — and runs
@@ -49,6 +51,10 @@ MAP = "c2"
 SHARED = False
 SHAPE_NAME = "c2: Qwen3-30B-A3B-shaped MoE layer (128 experts, top-8, d_h=2048, d_e=768, SwiGLU)"
 N_BATCHES = 8  # distinct routing batches rotated through the timed steps
+# `value` is the whole job (all N GPUs); BASELINE's tokens/s/GPU is a side field
+METRIC = "moe_layer_tokens_per_s"
+METRIC_NOTE = ("whole-job MoE-layer tokens/s over all n_gpus; BASELINE's MoE-layer "
+               "tokens/s/GPU is tokens_per_s_per_gpu = value / n_gpus")
 
 # --shape: the BASELINE configs' expert shapes (the default c2 is the headline;
 # the others are reported in profiles/, not the driver's scaling line)
@@ -314,7 +320,7 @@ def run_reference(args):
     tok_s = float(np.median([v["tok_s"] for v in vals]))
     c5 = c5_scheduler_cpu()
     line = {
-        "impl": "reference", "metric": "moe_layer_tokens_per_s_per_gpu", "value": tok_s,
+        "impl": "reference", "metric": METRIC, "value": tok_s,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic", "config": workload_config(T, args),
@@ -570,12 +576,13 @@ def run_ours(args):
         s5.close()
 
     line = {
-        "metric": "moe_layer_tokens_per_s_per_gpu", "value": value, "unit": "tokens/s",
+        "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (gen_batch Zipf routing, random-init bf16 weights)",
         "config": workload_config(T, args),
         "tokens_per_s_per_gpu": value / ws,
+        "value_is": METRIC_NOTE,
         "scheduler": {"us_per_iter": sched_us, "how": "CUDA-graph replay of 20 passes, median",
                       "cpu_schedule_us": cpu_sched[0], "cpu_schedule_reference_us": cpu_sched[1],
                       "c5": c5_line},
@@ -842,7 +849,7 @@ def run_box(args):
     timed_out = box.timed_out()
     if rank == 0:
         box_tok_s = T * args.steps / (ms_max / 1e3)
-        value = box_tok_s / ws  # per GPU of the box (all N, attention GPUs included)
+        value = box_tok_s  # the whole box (all N GPUs); per GPU in tokens_per_s_per_gpu
         sends = plan.bytes_per_step(T, D_H, 0 if args.gate else K_TOP)
         send_bytes = sends[0][0]
         hbm, tf_burst, tf_sus, src = peaks()
@@ -855,7 +862,7 @@ def run_box(args):
                 {"bound": "tensor", "achieved": tfs_slow, "peak": tf_peak, "unit": "TFLOP/s",
                  "frac": tfs_slow / tf_peak})
         line = {
-            "metric": "moe_layer_tokens_per_s_per_gpu", "value": value, "unit": "tokens/s",
+            "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
@@ -884,7 +891,8 @@ def run_box(args):
                                  "the rows",
                        "l2": "inputs > L2 (weights streamed)"},
             "tokens_per_s_box": box_tok_s, "tokens_per_s_per_moe_gpu": box_tok_s / M,
-            "value_is": "whole-box tokens/s / N GPUs (attention GPUs included; they run no "
+            "tokens_per_s_per_gpu": box_tok_s / ws,
+            "value_is": METRIC_NOTE + " (attention GPUs included in N; they run no "
                         "attention math here)",
             "roofline": {**roof, "kernel": "grouped_gemm_kernel on the slowest MoE GPU",
                          "ffn_us_per_step": ffn_ms * 1e3,
@@ -911,7 +919,7 @@ def run_box(args):
                        / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else None,
                        "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy "
                                                          "per direction (fallback)"},
-            "e2e": {"value": T * args.steps / e2e_s / ws, "unit": "tokens/s",
+            "e2e": {"value": T * args.steps / e2e_s, "unit": "tokens/s",
                     "h2d_bytes_per_step": T * (D_H * 2 + (0 if args.gate else K_TOP * 8)),
                     "d2h_bytes_per_step": T * D_H * 2},
             "scheduler": {"us_per_iter": sched_us, "slots": T * K_TOP,
