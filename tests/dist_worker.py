@@ -128,26 +128,41 @@ def main():
         box.combine(outs[step], Ts, step, stream)
 
     # one stream per rank; a colocated rank interleaves its roles in the same
-    # order as the split box's ranks would (dispatch before MoE before combine)
+    # order as the split box's ranks would (dispatch before MoE before combine).
+    # More ranks than GPUs: ranks sharing a GPU are separate processes, and no
+    # wait kernel may rely on another process's kernel running beside it — so
+    # every phase ends with a device sync and a barrier of all ranks, and each
+    # wait finds the flags it waits for already published.
+    def phase_end():
+        if ngpu:
+            torch.cuda.synchronize()
+            dist.barrier()
+
     if args.inflight == 1:
         for step in range(1, args.steps + 1):
             if att:
                 dispatch(step)
+            phase_end()
             if moe:
                 box.moe_step(steps[step - 1][0], step, stream)
+            phase_end()
             if att:
                 combine(step)
             torch.cuda.synchronize()
     else:
         if att:
             dispatch(1)
+        phase_end()
         for step in range(1, args.steps + 1):
             if att and step < args.steps:
                 dispatch(step + 1)
+            phase_end()
             if moe:
                 box.moe_step(steps[step - 1][0], step, stream)
+            phase_end()
             if att:
                 combine(step)
+            phase_end()
         torch.cuda.synchronize()
     for step in range(1, args.steps + 1):
         Ts, x, gw, ex = steps[step - 1]

@@ -127,7 +127,9 @@ def test_box_8_ranks_oversubscribed(box, transport):
     """The 8-rank boxes — MoE-only (the 8-GPU bench's default) and the
     north_star split 2A+6E (BASELINE c3) — as 8 processes on the GPUs there are
     (rank r on GPU r % n; CUDA IPC between processes, also on one device):
-    every shard vs the fp32 oracle, two steps in flight."""
+    every shard vs the fp32 oracle, two steps in flight.  Every phase ends
+    with a device sync and a barrier of all ranks, so no wait kernel relies on
+    a kernel of another process on its GPU running beside it."""
     n = max(1, min(gpus(), 8))
     out = tempfile.mkdtemp()
     roles = (["--attn", "8", "--moe", "8", "--colocated"] if box == "moe-only"
