@@ -193,6 +193,7 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->ffn.y);
   dfree(ctx->ffn.y2);
   dfree(ctx->ffn.tile_ctr);
+  dfree(ctx->gate_xchg);
   dfree(ctx->d_x);
   dfree(ctx->d_outbuf);
   dfree(ctx->d_experts);
@@ -1279,6 +1280,17 @@ janus_status janus_xfer_check(janus_ctx *ctx) {
                                          std::to_string(st) + ")");
 }
 
+// the gate's split-K exchange buffer: once per context, at its largest size
+// (bounded by the SM count), so no call allocates inside a stream capture after
+// the first
+static cudaError_t alloc_gate_xchg(janus_ctx *ctx) {
+  if (ctx->gate_xchg) return cudaSuccess;
+  int sms = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (e != cudaSuccess) return e;
+  return cudaMalloc(&ctx->gate_xchg, janus::gate_xchg_bytes(sms));
+}
+
 janus_status janus_gate_async(janus_ctx *ctx, const void *d_x, const void *d_router, int64_t T,
                               int d_hidden, int num_experts, int top_k, int32_t *d_experts,
                               float *d_gate_w, void *stream) {
@@ -1290,8 +1302,10 @@ janus_status janus_gate_async(janus_ctx *ctx, const void *d_x, const void *d_rou
                 "gate: need d_hidden % 64 == 0, 16 <= num_experts <= 256, num_experts % 16 == 0, "
                 "1 <= top_k <= min(16, num_experts)");
   CK(cudaSetDevice(ctx->device));
+  CK(alloc_gate_xchg(ctx));
   cudaError_t e = janus::launch_gate(d_x, d_router, (int)T, d_hidden, num_experts, top_k,
-                                     d_experts, d_gate_w, static_cast<cudaStream_t>(stream));
+                                     d_experts, d_gate_w, ctx->gate_xchg,
+                                     static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gate_kernel");
   if (T > 0) ctx->launches += 1;
   return JANUS_OK;
@@ -1300,6 +1314,8 @@ janus_status janus_gate_async(janus_ctx *ctx, const void *d_x, const void *d_rou
 janus_status janus_moe_set_router(janus_ctx *ctx, const void *d_router) {
   if (!ctx) return JANUS_EINVAL;
   if (!d_router) return fail(ctx, JANUS_EINVAL, "gate: null router");
+  CK(cudaSetDevice(ctx->device));
+  CK(alloc_gate_xchg(ctx));
   ctx->router = d_router;
   return JANUS_OK;
 }

@@ -7,16 +7,17 @@
 // ids are written in rank order, weights are softmax(top-k logits).
 //
 // One cluster of S CTAs per 128 tokens (UMMA M = 128, cta_group::1), N = E
-// (<= 256), K = d_h split S ways (S = 1, 2, 4 or 8, chosen so the grid covers
-// the SMs: at T = 4096 one CTA per token block would leave 116 SMs idle and
-// each CTA streaming 1 MB).  Each CTA runs its k-blocks through a TMA ring
+// (<= 256), K = d_h split S ways (S = 1, 2, 4 or 8: the largest that keeps
+// the grid one wave of resident clusters — at T = 4096 one CTA per token block
+// would leave 116 SMs idle and each CTA streaming 1 MB).  Each CTA runs its k-blocks through a TMA ring
 // into fp32 TMEM partial logits (one token per lane).  S = 1: each of 128
 // epilogue threads keeps a sorted top-KMAX list in registers while it streams
-// its token's E logits from TMEM.  S > 1: the partials are staged in smem and
-// bulk-copied (cp.async.bulk shared::cluster) to the CTA of the cluster that
-// owns the token (128/S tokens per CTA); the owner sums the S partials in
-// split order (deterministic), 2S threads per token each keep a top-KMAX of an
-// interleaved column subset, and a shuffle merge yields the token's top-k.
+// its token's E logits from TMEM.  S > 1: the partials are staged in smem,
+// bulk-stored to a global (L2-resident) exchange slot per CTA, and after a
+// cluster barrier the CTA that owns a token (128/S tokens per CTA) sums its S
+// partials in split order (deterministic); 2S threads per token each keep a
+// top-KMAX of an interleaved column subset, and a shuffle merge yields the
+// token's top-k.
 // HBM-bound: x is read once (2·d_h bytes per token), Wr (2·E·d_h) from L2.
 // Graph replay (c2 shape): 18.6 -> 12.6 us at T=256, 18.7 -> 14.8 us at
 // T=4096 against the one-CTA-per-token-block version; the rest is the
@@ -47,6 +48,7 @@ struct GateParams {
   int stages;        // ring depth
   int32_t *experts;  // [T*k]
   float *gw;         // [T*k]
+  float *xchg;       // S > 1: [chunks][grid][128][ld] partial logits (global, L2-resident)
 };
 
 __device__ __forceinline__ void tma_load(void *dst, const CUtensorMap *tm, uint64_t *bar, int x,
@@ -90,29 +92,30 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ uint32_t gate_mapa(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, const float *v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3])
+               : "memory");
 }
 __device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, const float *v) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v[0]), "f"(v[1]),
-               "f"(v[2]), "f"(v[3])
-               : "memory");
-}
-// smem -> (peer) smem bulk copy, completing `bytes` on the destination's mbarrier
-__device__ __forceinline__ void bulk_copy_cluster(uint32_t cl_dst, uint32_t src, uint32_t bytes,
-                                                  uint32_t cl_bar) {
+// global -> own smem bulk copy, completing `bytes` on the mbarrier
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes,
+                                          uint64_t *bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          cl_dst),
-      "r"(src), "r"(bytes), "r"(cl_bar)
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// smem -> global bulk copy (async proxy), tracked by the bulk-group counter
+__device__ __forceinline__ void bulk_store(void *dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes)
+               : "memory");
 }
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
@@ -288,23 +291,28 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
   }
 
   // ---- S > 1: exchange the partial logits, sum in split order, top-k ----
-  // The E columns go in chunks of <= 128 (smem: staging + receive buffer,
-  // both in the dead ring).  Per chunk: warps 2-5 stage their token rows
-  // (thread = TMEM lane) into stg[128][ld]; after a cluster barrier one
-  // thread bulk-copies rows [j*R, (j+1)*R) to CTA j's recv[split]
-  // (complete_tx on CTA j's mbarrier).  Then G = 256/R threads per owned
-  // token sum the S partials in split order and insert their columns sub,
-  // sub+G, ... into a top-KMAX list; after the last chunk the G lists merge.
+  // The E columns go in chunks of <= 128.  Per chunk: warps 2-5 stage their
+  // token rows (thread = TMEM lane) into stg[128][ld] in the dead ring; one
+  // thread bulk-stores the whole block to this CTA's slot of the global
+  // exchange buffer (L2) and waits for it; after a cluster barrier the owner
+  // of tokens [split*R, (split+1)*R) bulk-loads their rows of the S slots of
+  // its cluster into recv[S][R][ld] (one L2 round trip), and G = 256/R
+  // threads per owned token sum them in split order, inserting columns sub,
+  // sub+G, ... into a top-KMAX list; after the last chunk the G lists merge.  (The exchange through DSMEM bulk copies moved
+  // ~17-21 B/clk per SM, 1.4-4.7 us per chunk at T = 4096; L2 is several
+  // times that.)
   if (S > 1) {
     const int R = kGateM / S;        // tokens owned by this CTA
     const int G = kGateThreads / R;  // threads per token (2S)
     const int nch = (p.E + 127) / 128;
     const int EC = ((p.E + nch - 1) / nch + 15) & ~15;  // chunk width
-    const int ld = EC + G;           // row stride (floats): conflict-free sums
+    const int ld = EC + G;           // row stride (floats)
     const uint32_t stg = smem_u32(smem);
     const uint32_t recv = stg + (uint32_t)(kGateM * ld) * 4u;
-    const uint32_t chunk_bytes = (uint32_t)(R * ld) * 4u;  // per (source, destination)
+    const uint32_t part = (uint32_t)(R * ld) * 4u;  // bytes of one slot's owned rows
+    const size_t slot = (size_t)kGateM * ld;  // floats per CTA slot
     const int tok = threadIdx.x / G, sub = threadIdx.x % G;
+    const int first = blockIdx.x - (int)split;  // the cluster's first CTA
     float val[KMAX];
     int idx[KMAX];
 #pragma unroll
@@ -314,9 +322,10 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
     }
     for (int c = 0; c < nch; ++c) {
       const int c0 = c * EC, c1 = min(p.E, c0 + EC);
-      if (c > 0) {  // this CTA's copies have read stg; every CTA is done with its recv
+      float *xc = p.xchg + (size_t)c * gridDim.x * slot;
+      if (c > 0) {  // the previous chunk's bulk store has read stg, every thread recv
         if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        cluster_barrier();
+        __syncthreads();
       }
       if (warp >= 2 && warp < 6) {
         const int quad = warp & 3, row = quad * 32 + lane;
@@ -328,16 +337,22 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
           for (int q = 0; q < 32; q += 4)
             if (e0 + q < c1) st_shared_v4(dst + (uint32_t)(e0 - c0 + q) * 4u, v + q);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging -> bulk copies
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging -> bulk store
       }
-      if (threadIdx.x == 0) mbar_expect_tx(recv_bar, (uint32_t)S * chunk_bytes);
-      cluster_barrier();  // every CTA's staging is written and its expect_tx armed
+      __syncthreads();
       if (threadIdx.x == 0) {
-        for (int j = 0; j < S; ++j)
-          bulk_copy_cluster(gate_mapa(recv + split * chunk_bytes, (uint32_t)j),
-                            stg + (uint32_t)j * chunk_bytes, chunk_bytes,
-                            gate_mapa(smem_u32(recv_bar), (uint32_t)j));
+        bulk_store(xc + (size_t)blockIdx.x * slot, stg, (uint32_t)(slot * 4));
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // written, not just read
+        asm volatile("fence.proxy.async.global;" ::: "memory");    // async writes -> generic reads
+      }
+      cluster_barrier();  // every CTA's slot of this chunk is in global memory
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // barrier -> async reads
+        mbar_expect_tx(recv_bar, (uint32_t)S * part);
+        for (int j = 0; j < S; ++j)
+          bulk_load(recv + (uint32_t)j * part, xc + (size_t)(first + j) * slot + (size_t)split * R * ld,
+                    part, recv_bar);
       }
       mbar_wait(recv_bar, (uint32_t)c & 1);
       // recv[s][tok][e - c0]: split s's partial logit of owned token tok
@@ -347,7 +362,7 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
         float x = ld_shared_f32(a);
 #pragma unroll
         for (int s = 1; s < 8; ++s)
-          if (s < S) x += ld_shared_f32(a + (uint32_t)s * chunk_bytes);
+          if (s < S) x += ld_shared_f32(a + (uint32_t)s * part);
         topk_insert(val, idx, x, e);
       }
     }
@@ -359,12 +374,7 @@ __global__ void __launch_bounds__(kGateThreads, 1) gate_kernel(const __grid_cons
   }
 
   tc_fence_before();
-  if (S > 1) {  // no CTA leaves while a peer may still address its smem
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    cluster_barrier();
-  } else {
-    __syncthreads();
-  }
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
@@ -386,18 +396,43 @@ cudaError_t launch_gate_k(const GateParams &g, size_t smem, cudaStream_t s) {
   }
   const int blocks = (g.T + kGateM - 1) / kGateM;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(blocks * g.splits);
   cfg.blockDim = dim3(kGateThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = g.splits;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gate_kernel<KMAX>, g);
+  // clusters of n CTAs resident at once (GPC-bound: fewer than SMs / n for
+  // n = 4, 8), per device and shared-memory size
+  static int occ_dev = -1;
+  static size_t occ_smem = 0;
+  static int occ[4] = {0, 0, 0, 0};  // n = 1, 2, 4, 8
+  if (occ_dev != dev || occ_smem != smem) {
+    for (int i = 0; i < 4; ++i) {
+      attr[0].val.clusterDim.x = 1u << i;
+      cfg.gridDim = dim3(1u << i);
+      cudaError_t e = cudaOccupancyMaxActiveClusters(&occ[i], gate_kernel<KMAX>, &cfg);
+      if (e != cudaSuccess) return e;
+    }
+    occ_dev = dev;
+    occ_smem = smem;
+  }
+  // split K S ways while every cluster of the grid is resident at once (one
+  // wave) and each CTA keeps >= 2 k-blocks
+  int S = 1, lg = 0;
+  while (S < 8 && blocks <= occ[lg + 1] && g.K / kGBK >= 4 * S) {
+    S *= 2;
+    ++lg;
+  }
+  if (S > 1 && !g.xchg) return cudaErrorInvalidValue;
+  GateParams gs = g;
+  gs.splits = S;
+  attr[0].val.clusterDim.x = S;
+  cfg.gridDim = dim3(blocks * S);
+  return cudaLaunchKernelEx(&cfg, gate_kernel<KMAX>, gs);
 }
 
 }  // namespace
@@ -407,8 +442,12 @@ bool gate_shape_ok(int d_h, int E, int k) {
          k <= E;
 }
 
+size_t gate_xchg_bytes(int sms) {  // S > 1 only while the grid is one wave
+  return (size_t)2 * sms * kGateM * (128 + 16) * sizeof(float);
+}
+
 cudaError_t launch_gate(const void *x, const void *wr, int T, int d_h, int E, int k,
-                        int32_t *experts, float *gw, cudaStream_t s) {
+                        int32_t *experts, float *gw, float *xchg, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   GateParams g{};
   if (!make_map(&g.tm_x, x, (uint64_t)T, (uint64_t)d_h, kGateM) ||
@@ -420,15 +459,9 @@ cudaError_t launch_gate(const void *x, const void *wr, int T, int d_h, int E, in
   g.k = k;
   g.experts = experts;
   g.gw = gw;
-  // split K S ways while the grid still fits the SMs (each CTA keeps >= 2 k-blocks)
-  int sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int blocks = (T + kGateM - 1) / kGateM, kblocks = d_h / kGBK;
-  int S = 1;
-  while (S < 8 && blocks * S * 2 <= sms && kblocks >= 4 * S) S *= 2;
+  g.xchg = xchg;
+  // the K split S is chosen at launch (launch_gate_k: one wave of clusters)
   const int stage_bytes = kGateM * kGBK * 2 + E * kGBK * 2;
-  g.splits = S;
   g.stages = std::min(kGMaxStages, kGRingBytes / stage_bytes);
   const size_t smem = (size_t)g.stages * stage_bytes + 1024 + 256;
   if (k <= 4) return launch_gate_k<4>(g, smem, s);

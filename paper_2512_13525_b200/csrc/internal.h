@@ -126,8 +126,10 @@ cudaError_t launch_combine(const void *y, const int32_t *slot_row, const int32_t
 
 // MoE-side gating (gate.cu): router GEMM + top-k + softmax of the top-k logits.
 bool gate_shape_ok(int d_h, int E, int k);
+// xchg: the split-K exchange buffer, gate_xchg_bytes(SM count) bytes
+size_t gate_xchg_bytes(int sms);
 cudaError_t launch_gate(const void *x, const void *wr, int T, int d_h, int E, int k,
-                        int32_t *experts, float *gw, cudaStream_t s);
+                        int32_t *experts, float *gw, float *xchg, cudaStream_t s);
 
 // GPU activation statistics (stats.cu): ActivationStats on the device.
 struct StatsState {
@@ -315,6 +317,7 @@ struct janus_ctx {
   int32_t *d_experts = nullptr;
   float *d_gw = nullptr;
   const void *router = nullptr;  // [E][d_h] bf16 (janus_moe_set_router; caller-owned)
+  float *gate_xchg = nullptr;    // the gate's split-K exchange buffer (allocated on first use)
 
   // CUDA-graph replay of the single-GPU layer (janus_moe_layer_async)
   struct GraphKey {
