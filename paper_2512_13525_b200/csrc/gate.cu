@@ -19,9 +19,10 @@
 // top-KMAX of an interleaved column subset, and a shuffle merge yields the
 // token's top-k.
 // HBM-bound: x is read once (2·d_h bytes per token), Wr (2·E·d_h) from L2.
-// Graph replay (c2 shape): 18.6 -> 12.6 us at T=256, 18.7 -> 14.8 us at
-// T=4096 against the one-CTA-per-token-block version; the rest is the
-// per-element top-k insertion (issue-bound) and the cluster exchange.
+// Graph replay (c2 shape): 18.6 -> 12.6 -> 10.8 us at T=256, 18.7 -> 14.8 ->
+// 12.7 us at T=4096 (one CTA per token block -> split K with a DSMEM exchange
+// -> the exchange through L2); the rest is the load -> MMA -> exchange ->
+// top-k chain of one token block and the cluster barriers.
 #include <cuda_bf16.h>
 
 #include <algorithm>
