@@ -605,6 +605,41 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def box_trace(box, run_steps, s, s_moe, att, moe, rank, epoch, n=30):
+    """JANUS_BOX_TRACE=1: the pipelined box loop again with CUDA events around
+    every enqueued call (dispatch / combine on the attention stream, the MoE
+    step on its own), written to gpurun_out/boxtrace_rank{r}.json — when each
+    stream reached and finished each call, relative to the first event."""
+    import torch
+    import torch.distributed as dist
+    orig = (box.dispatch, box.moe_step, box.combine)
+    evs = []
+
+    def wrap(name, fn, st):
+        def f(*a):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn(*a)
+            e1.record(st)
+            evs.append((name, int(a[-2]), e0, e1))
+        return f
+    box.dispatch = wrap("dispatch", orig[0], s)
+    box.moe_step = wrap("moe", orig[1], s_moe)
+    box.combine = wrap("combine", orig[2], s)
+    torch.cuda.synchronize()
+    dist.barrier()
+    base = torch.cuda.Event(enable_timing=True)
+    base.record(s)
+    run_steps(n)
+    torch.cuda.synchronize()
+    box.dispatch, box.moe_step, box.combine = orig
+    rows = [(nm, ep, base.elapsed_time(a), base.elapsed_time(b)) for nm, ep, a, b in evs]
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(f"gpurun_out/boxtrace_rank{rank}.json", "w") as f:
+        json.dump(rows, f)
+    dist.barrier()
+
+
 def run_box(args):
     """N > 1: one NVLink box.  Default (``--box moe-only``): every GPU owns a
     token shard AND is an MoE instance (the attention and MoE sub-groups are
@@ -710,6 +745,8 @@ def run_box(args):
         lib.janus_profile_read(layer.ctx, C.byref(a_), C.byref(b_), C.byref(c_))
         lib.janus_profile(layer.ctx, 0)
         ffn = [a_.value / max(c_.value, 1), b_.value / max(c_.value, 1), 1.0]
+    if os.environ.get("JANUS_BOX_TRACE"):  # diagnostics: per-call events of the pipelined loop
+        box_trace(box, run_steps, s, s_moe, att, moe, rank, epoch)
     # dispatch kernel alone (attention ranks): events around the dispatch only,
     # over extra steps after the timed region
     # each phase alone, one step in flight: attention dispatch; MoE step (from
