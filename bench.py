@@ -706,6 +706,11 @@ def run_box(args):
     # not hold back its MoE step i+1
     s_moe = torch.cuda.Stream(dev) if plan.colocated else s
     stream_moe = s_moe.cuda_stream
+    # combines on their own stream: a dispatch is not queued behind the previous
+    # step's combine (which waits for every rank's partial-sum push); the
+    # library keeps the epoch slots safe by events and flags (three slots)
+    s_comb = torch.cuda.Stream(dev)
+    stream_comb = s_comb.cuda_stream
     epoch = [0]
 
     # Two steps in flight (the exchange double-buffers by epoch parity): an
@@ -722,7 +727,7 @@ def run_box(args):
             if moe:
                 box.moe_step(T, e0_ + j + 1, stream_moe)
             if att:
-                box.combine(out, T, e0_ + j + 1, stream)
+                box.combine(out, T, e0_ + j + 1, stream_comb)
         epoch[0] += n
 
     run_steps(args.warmup)

@@ -169,9 +169,13 @@ void janus_destroy(janus_ctx *ctx) {
     for (int i = 0; i < 2; ++i) {
       if (x.ffn_done[i]) cudaEventDestroy(x.ffn_done[i]);
       if (x.push_done[i]) cudaEventDestroy(x.push_done[i]);
+      x.ffn_done[i] = x.push_done[i] = nullptr;
+    }
+    for (int i = 0; i < janus::kXferSlots; ++i) {
       if (x.own_disp[i]) cudaEventDestroy(x.own_disp[i]);
       if (x.own_sig[i]) cudaEventDestroy(x.own_sig[i]);
-      x.ffn_done[i] = x.push_done[i] = x.own_disp[i] = x.own_sig[i] = nullptr;
+      if (x.comb_done[i]) cudaEventDestroy(x.comb_done[i]);
+      x.own_disp[i] = x.own_sig[i] = x.comb_done[i] = nullptr;
     }
     for (cudaStream_t st : x.ce_streams) {
       cudaStreamSynchronize(st);
@@ -211,7 +215,7 @@ void janus_destroy(janus_ctx *ctx) {
   dfree(ctx->xfer.err);
   free_assign(ctx->xfer.rws);
   dfree(ctx->xfer.dmask);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < janus::kXferSlots; ++i) {
     free_assign(ctx->xfer.lay[i]);
     dfree(ctx->xfer.lay_tile[i]);
   }
@@ -783,11 +787,11 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
   int launches = 0;
   if (ev) CK(cudaEventRecord(ev[2], s));
   // the colocated routed MoE role pushes its partial sums on a side stream
-  // over y[epoch slot], beside the next step's permute and GEMMs (measured:
-  // the push is ~85 us of a 4-GPU step); the GEMMs that write y[slot] again
+  // over y[epoch parity], beside the next step's permute and GEMMs (measured:
+  // the push is ~85 us of a 4-GPU step); the GEMMs that write y[parity] again
   // two steps later wait for that push
   const janus::XferState &xs = ctx->xfer;
-  const int psl = (int)janus::xfer_slot(push_epoch);
+  const int psl = (int)(push_epoch & 1);
   const bool side_push = push_epoch && pre && !shared && !xs.mc && xs.push_stream && p.y2 &&
                          xs.transport == janus::kXferRouted && !xs.local_connect;
   if (side_push) CK(cudaStreamWaitEvent(s, xs.push_done[psl], 0));
@@ -821,7 +825,8 @@ static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_
                                   a.status, &pd, push_blocks());
         if (e == cudaSuccess) e = janus::launch_signal_combine(x, a.status, push_epoch, x.push_stream);
         if (e == cudaSuccess) e = cudaEventRecord(x.push_done[psl], x.push_stream);
-        if (e == cudaSuccess && x.own_sig[psl]) e = cudaEventRecord(x.own_sig[psl], x.push_stream);
+        const cudaEvent_t own = x.own_sig[janus::xfer_slot(push_epoch)];
+        if (e == cudaSuccess && own) e = cudaEventRecord(own, x.push_stream);
         launches += 1;
         if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_kernel");
         ctx->launches += 2 + launches;
@@ -905,7 +910,7 @@ static void xfer_release(janus_ctx *ctx) {
   dfree(x.err);
   free_assign(x.rws);
   dfree(x.dmask);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < janus::kXferSlots; ++i) {
     free_assign(x.lay[i]);
     dfree(x.lay_tile[i]);
   }
@@ -916,8 +921,11 @@ static void xfer_release(janus_ctx *ctx) {
   for (int i = 0; i < 2; ++i) {
     if (x.ffn_done[i]) cudaEventDestroy(x.ffn_done[i]);
     if (x.push_done[i]) cudaEventDestroy(x.push_done[i]);
+  }
+  for (int i = 0; i < janus::kXferSlots; ++i) {
     if (x.own_disp[i]) cudaEventDestroy(x.own_disp[i]);
     if (x.own_sig[i]) cudaEventDestroy(x.own_sig[i]);
+    if (x.comb_done[i]) cudaEventDestroy(x.comb_done[i]);
   }
   for (cudaStream_t st : x.ce_streams) cudaStreamDestroy(st);
   for (cudaEvent_t ev : x.ce_done) cudaEventDestroy(ev);
@@ -949,17 +957,19 @@ static janus_status xfer_setup(janus_ctx *ctx, int n_attn, int n_moe, int rank, 
   x.L = janus::xfer_layout(n_attn, n_moe, max_tokens, d_h, k);
   CK(cudaMalloc(&x.local, x.L.bytes));
   CK(cudaMemset(x.local, 0, x.L.bytes));
-  CK(dalloc(&x.counter, 2 * janus::kCounterKinds));
+  CK(dalloc(&x.counter, janus::kXferSlots * janus::kCounterKinds));
   CK(dalloc(&x.err, janus::kErrWords));
-  CK(cudaMemset(x.counter, 0, sizeof(unsigned) * 2 * janus::kCounterKinds));
+  CK(cudaMemset(x.counter, 0, sizeof(unsigned) * janus::kXferSlots * janus::kCounterKinds));
   CK(cudaMemset(x.err, 0, sizeof(int) * janus::kErrWords));
   x.peer_base.assign(x.world, nullptr);
   x.peer_base[rank] = x.local;
-  if (colocated)
-    for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < janus::kXferSlots; ++i) {
+    if (colocated) {
       CK(cudaEventCreateWithFlags(&x.own_disp[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&x.own_sig[i], cudaEventDisableTiming));
     }
+    if (rank < n_attn) CK(cudaEventCreateWithFlags(&x.comb_done[i], cudaEventDisableTiming));
+  }
   return JANUS_OK;
 }
 
@@ -1004,10 +1014,10 @@ janus_status janus_xfer_set_transport(janus_ctx *ctx, int transport) {
     // the destination masks of its tokens, per epoch slot
     CK(alloc_assign(x.rws, (int)std::min<long long>(x.T_max * x.k, INT_MAX), JANUS_MAX_EXPERTS,
                     JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
-    CK(dalloc(&x.dmask, 2 * x.L.ta_max));
-    CK(cudaMemset(x.dmask, 0, sizeof(uint32_t) * 2 * x.L.ta_max));
+    CK(dalloc(&x.dmask, janus::kXferSlots * x.L.ta_max));
+    CK(cudaMemset(x.dmask, 0, sizeof(uint32_t) * janus::kXferSlots * x.L.ta_max));
     if (x.moe0 == 0 && ctx->ffn.h) {  // colocated with a configured layer: one K1 per step
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < janus::kXferSlots; ++i) {
         CK(alloc_assign(x.lay[i], (int)std::min<long long>(x.T_max * x.k, INT_MAX),
                         JANUS_MAX_EXPERTS, JANUS_MAX_INSTANCES, JANUS_MAX_REPLICAS));
         CK(dalloc(&x.lay_tile[i], JANUS_MAX_REPLICAS + 1));
@@ -1095,6 +1105,28 @@ janus_status janus_xfer_connect_local(janus_ctx *ctx, janus_ctx *const *peers) {
   return JANUS_OK;
 }
 
+// A dispatch (or routing push) into epoch slot e % kXferSlots reuses the slot
+// of epoch e - kXferSlots: every MoE rank must have finished that step (its
+// partial sums pushed — it no longer reads the rows, routing or layout there)
+// and this rank's own combine must have summed the partials the slot holds.
+// Stream order gives both when dispatch and combine share one stream; this
+// makes a dispatch on a stream of its own safe: the combine by its event, the
+// own MoE role by its event, the other MoE ranks by their combine flags (a
+// wait kernel spinning on other GPUs only).  Once per epoch.
+static janus_status slot_free_wait(janus_ctx *ctx, uint64_t epoch, cudaStream_t s) {
+  janus::XferState &x = ctx->xfer;
+  if (epoch <= (uint64_t)janus::kXferSlots || x.slot_epoch == epoch) return JANUS_OK;
+  const size_t sl = janus::xfer_slot(epoch);
+  if (x.comb_done[sl]) CK(cudaStreamWaitEvent(s, x.comb_done[sl], 0));
+  const cudaEvent_t own = x.own_sig[sl];
+  if (own) CK(cudaStreamWaitEvent(s, own, 0));
+  cudaError_t e = janus::launch_wait(x, 3, epoch - janus::kXferSlots, s, own ? x.rank - x.moe0 : -1);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
+  ctx->launches += 1;
+  x.slot_epoch = epoch;
+  return JANUS_OK;
+}
+
 janus_status janus_attn_route_async(janus_ctx *ctx, const int32_t *d_experts, const float *d_gate_w,
                                     int64_t T, uint64_t epoch, void *stream) {
   if (!ctx || !ctx->xfer_ready) return fail(ctx, JANUS_ESTATE, "xfer: not connected");
@@ -1104,6 +1136,8 @@ janus_status janus_attn_route_async(janus_ctx *ctx, const int32_t *d_experts, co
     return fail(ctx, JANUS_ESTATE, "xfer: routing phase of the routed transport only");
   if (T < 0 || T > x.T_max || epoch == 0 || !d_experts || !d_gate_w)
     return fail(ctx, JANUS_EINVAL, "xfer: num_tokens outside [0, max_tokens], epoch 0 or no routing");
+  janus_status st = slot_free_wait(ctx, epoch, static_cast<cudaStream_t>(stream));
+  if (st != JANUS_OK) return st;
   cudaError_t e = janus::launch_route_push(x, d_experts, d_gate_w, T, epoch,
                                            static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(ctx, e, "route_push_kernel");
@@ -1123,6 +1157,8 @@ janus_status janus_attn_dispatch_async(janus_ctx *ctx, const void *d_x, const in
   if (!d_experts != !d_gate_w)
     return fail(ctx, JANUS_EINVAL, "xfer: pass both routing arrays, or neither (MoE-side gating)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  janus_status fs = slot_free_wait(ctx, epoch, s);
+  if (fs != JANUS_OK) return fs;
   // a colocated rank's MoE role waits for this dispatch by an event
   const cudaEvent_t own = x.own_disp[janus::xfer_slot(epoch)];
   if (x.transport == janus::kXferCE) {  // copy engines: no kernel
@@ -1247,6 +1283,9 @@ janus_status janus_attn_combine_async(janus_ctx *ctx, void *d_out, int64_t T, ui
                             : janus::launch_reduce_partials(x, d_out, Ta, epoch, s);
   if (e != cudaSuccess)
     return cuda_fail(ctx, e, x.mc && x.mc_reduce ? "reduce_mc_kernel" : "reduce_partials_kernel");
+  // the slot's next dispatch (kXferSlots epochs on) waits for this combine
+  if (x.comb_done[janus::xfer_slot(epoch)])
+    CK(cudaEventRecord(x.comb_done[janus::xfer_slot(epoch)], s));
   ctx->launches += 2;
   return JANUS_OK;
 }

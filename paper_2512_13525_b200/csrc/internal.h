@@ -144,6 +144,12 @@ struct StatsState {
 cudaError_t launch_stats_record(const StatsState &st, const int32_t *experts, long long S,
                                 cudaStream_t s);
 
+// Epoch slots of the exchange: three, so the dispatch of step s+1 can run
+// while step s computes and step s-1's partial sums are still in flight
+// (dispatch and combine on different streams); a dispatch into a slot waits
+// until every MoE rank's push of the epoch kXferSlots back has landed.
+constexpr int kXferSlots = 3;
+
 // Attention <-> MoE exchange (xfer.cu).  Ranks [0, A) own token shards,
 // ranks [A, A+M) are MoE instances g = rank - A.  One exchange region per
 // rank, identical layout everywhere.
@@ -151,8 +157,10 @@ struct XferLayout {
   // flags (u64, epoch-valued): dispatch[A] (rows landed), combine[M] (partial
   // sums landed), route[A] (routing landed; routed transport).
   size_t flag_dispatch_off, flag_combine_off, flag_route_off;
-  // x/ex/gw/part/err offsets are slot 0's; slot 1 (odd epochs) is + slot_stride,
-  // so two steps can be in flight (dispatch of step s+1 while step s computes).
+  // x/ex/gw/part/err offsets are slot 0's; slot i (epoch % kXferSlots == i) is
+  // + i * slot_stride, so a dispatch can run ahead of the previous steps'
+  // combines (dispatch of step s+1 while step s computes and step s-1's
+  // partial sums are still being pushed and summed).
   // err[M] = {status, bad expert} of MoE instance g's step, written before its
   // combine flag (a failed MoE step is reported on the attention ranks).
   size_t x_off, ex_off, gw_off, part_off, err_off, slot_stride, bytes;
@@ -171,7 +179,7 @@ enum XferErr {
   kErrTimeout = 0,  // sticky: a bounded wait expired
   kErrStatus = 1,   // sticky: first failed step's status (a remote MoE step's, or this rank's)
   kErrBad = 2,      // sticky: its bad expert id
-  kErrSkip = 3,     // + wait kind (0 dispatch, 1 combine, 2 route): this step's verdict of
+  kErrSkip = 3,     // + wait kind (0 dispatch, 1 combine, 2 route, 3 slot free): this step's verdict of
                     // that wait, 1 -> the step's later kernels skip their work
   kErrWords = 8
 };
@@ -187,20 +195,21 @@ struct XferState {
   void *local = nullptr;              // this rank's exchange region
   std::vector<void *> peer_base;      // every rank's region (mapped), by rank
   std::vector<void *> opened;         // IPC mappings to close
-  unsigned *counter = nullptr;        // last-block counters [kinds][2 epoch slots] (device)
+  unsigned *counter = nullptr;        // last-block counters [kinds][kXferSlots] (device)
   int *err = nullptr;                 // XferErr words (device)
   int transport = kXferP2P;
   unsigned long long routed_epoch = 0;  // routed: routing of this epoch already pushed
+  unsigned long long slot_epoch = 0;    // the slot-free wait of this epoch already enqueued
   // routed transport, attention side: the step's schedule (K1 over every
   // shard's routing) and each owned token's destination-instance mask per
-  // epoch slot ([2][ta_max])
+  // epoch slot ([kXferSlots][ta_max])
   janus_assignment rws{};
   uint32_t *dmask = nullptr;
   // colocated routed ranks: the attention role's K1 writes the whole layout of
   // the step per epoch slot, and the rank's MoE role runs on it (one K1 per
   // step per GPU instead of two)
-  janus_assignment lay[2] = {};
-  int32_t *lay_tile[2] = {nullptr, nullptr};
+  janus_assignment lay[kXferSlots] = {};
+  int32_t *lay_tile[kXferSlots] = {};
   // NVLS multicast transport (mc.cpp): the bulk rows / routing / partial sums
   // go through one multicast object; flags stay in the IPC regions above.
   bool mc = false, mc_bound = false;
@@ -212,7 +221,7 @@ struct XferState {
   unsigned long long mc_handle = 0, mem_handle = 0;  // CUmemGenericAllocationHandle
   unsigned long long mc_va = 0, uc_va = 0;           // multicast / own-backing mappings
   size_t mc_bytes = 0, mc_gran = 0;
-  size_t mx_off = 0, mex_off = 0, mgw_off = 0, mpart_off = 0, mslot = 0;  // slot 0; slot 1 = + mslot
+  size_t mx_off = 0, mex_off = 0, mgw_off = 0, mpart_off = 0, mslot = 0;  // slot 0; slot i = + i * mslot
   // copy-engine transport: one stream per MoE rank (the copies to different
   // ranks run on different engines at once), forked from / joined into the
   // caller's stream
@@ -221,14 +230,18 @@ struct XferState {
   cudaEvent_t ce_fork = nullptr;
   // colocated routed MoE role: step s's partial-sum push (K5 + signal) runs on
   // push_stream, beside step s+1's permute and GEMMs (ffn_done / push_done per
-  // epoch slot order it after its GEMMs and the GEMMs two steps later after it)
+  // y buffer (epoch parity) order it after its GEMMs and the GEMMs two steps
+  // later after it)
   cudaStream_t push_stream = nullptr;
   cudaEvent_t ffn_done[2] = {nullptr, nullptr}, push_done[2] = {nullptr, nullptr};
   // a colocated rank's two roles run on different streams of one GPU: the MoE
   // role orders itself after its own attention role's dispatch, and the
   // attention role's combine after its own MoE role's signal, by these events
   // (per epoch slot) — it spins only on the other GPUs' flags
-  cudaEvent_t own_disp[2] = {nullptr, nullptr}, own_sig[2] = {nullptr, nullptr};
+  cudaEvent_t own_disp[kXferSlots] = {}, own_sig[kXferSlots] = {};
+  // attention ranks: the combine of each epoch slot done (a dispatch into the
+  // slot waits for the combine kXferSlots epochs back, whatever stream it ran on)
+  cudaEvent_t comb_done[kXferSlots] = {};
   bool local_connect = false;  // every rank in this process (janus_xfer_connect_local)
 };
 constexpr int kCounterKinds = 2;  // 0: row dispatch, 1: routing push
@@ -239,7 +252,7 @@ std::string mc_join(XferState &x, int device, int fd);     // other ranks
 std::string mc_bind(XferState &x, int device);             // every rank, after all joined
 void mc_free(XferState &x, int device);
 
-inline size_t xfer_slot(unsigned long long epoch) { return (size_t)(epoch & 1); }
+inline size_t xfer_slot(unsigned long long epoch) { return (size_t)(epoch % kXferSlots); }
 // Attention rank: broadcast dispatch — shard rows (+ routing) into every MoE
 // rank (P2P) or the multicast mapping (NVLS); flag_dispatch.
 cudaError_t launch_dispatch(const XferState &x, const void *d_x, const int32_t *d_ex,

@@ -122,8 +122,8 @@ std::string plan_layout(XferState &x, int device) {
   x.mex_off = take((size_t)x.T_max * x.k * 4);
   x.mgw_off = take((size_t)x.T_max * x.k * 4);
   x.mpart_off = take((size_t)x.T_max * x.d_h * 2);
-  x.mslot = o;  // two slots: steps of odd epochs use the second
-  x.mc_bytes = 2 * o;
+  x.mslot = o;  // kXferSlots slots: epoch % kXferSlots
+  x.mc_bytes = kXferSlots * o;
   CUmulticastObjectProp mp = mc_prop(x);
   size_t g1 = 0, g2 = 0;
   CU_TRY(d.mcGranularity(&g1, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED), "granularity");

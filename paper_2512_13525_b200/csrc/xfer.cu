@@ -369,7 +369,7 @@ void shard_host(const XferState &x, long long T, long long &first, long long &Ta
 }
 
 unsigned *counter_for(const XferState &x, int kind, unsigned long long epoch) {
-  return x.counter + 2 * kind + xfer_slot(epoch);
+  return x.counter + kXferSlots * kind + xfer_slot(epoch);
 }
 
 }  // namespace
@@ -412,7 +412,7 @@ XferLayout xfer_layout(int A, int M, long long T_max, int d_h, int k) {
   L.err_off = o;
   o = up(o + 8 * (size_t)M);
   L.slot_stride = o - slot0;
-  L.bytes = o + L.slot_stride;
+  L.bytes = o + (kXferSlots - 1) * L.slot_stride;
   L.ta_max = ta_max;
   return L;
 }
@@ -538,9 +538,12 @@ cudaError_t launch_routed_dispatch(const XferState &x, const void *d_x, const in
 cudaError_t launch_wait(const XferState &x, int kind, unsigned long long epoch, cudaStream_t s,
                         int skip) {
   unsigned char *base = static_cast<unsigned char *>(x.local);
+  // kind 3: the combine flags again, for the slot-free wait of a dispatch
+  // (its own skip word; errors are the combine's to report)
   const size_t off = kind == 0 ? x.L.flag_dispatch_off
-                               : kind == 1 ? x.L.flag_combine_off : x.L.flag_route_off;
-  const int n = kind == 1 ? x.M : x.A;
+                     : kind == 1 || kind == 3 ? x.L.flag_combine_off
+                                              : x.L.flag_route_off;
+  const int n = kind == 1 || kind == 3 ? x.M : x.A;
   const int2 *errs =
       kind == 1 ? reinterpret_cast<const int2 *>(base + x.L.err_off + xfer_slot(epoch) * x.L.slot_stride)
                 : nullptr;

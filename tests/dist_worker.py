@@ -49,6 +49,8 @@ def main():
                     help="MoE-side gating: dispatch rows only, MoE ranks run the router")
     ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
                     help="2: dispatch step s+1 before combining step s (double-buffered slots)")
+    ap.add_argument("--split-streams", action="store_true",
+                    help="combines on a stream of their own (the slots kept safe by the library)")
     args = ap.parse_args()
     rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     # JANUS_TEST_GPUS=n: more ranks than GPUs (rank r on GPU r % n; the
@@ -100,6 +102,10 @@ def main():
         return wcache[e]
 
     stream = torch.cuda.current_stream(dev).cuda_stream
+    # --split-streams: as bench.py runs the box — dispatch, MoE step and combine
+    # each on a stream of its own
+    cstream = torch.cuda.Stream(dev).cuda_stream if args.split_streams else stream
+    mstream = torch.cuda.Stream(dev).cuda_stream if args.split_streams else stream
     result = {"rank": rank, "role": plan.role(rank), "steps": [], "transport": box.transport}
     steps = []
     for step in range(1, args.steps + 1):
@@ -110,6 +116,10 @@ def main():
         steps.append((Ts, x, gw, ex))
 
     outs = {}
+    for step in range(1, args.steps + 1 if att else 1):  # made before any stream uses them
+        first, cnt = plan.shard(steps[step - 1][0], rank)
+        outs[step] = torch.empty(cnt, d_h, dtype=torch.bfloat16, device=dev)
+    torch.cuda.synchronize()
 
     def dispatch(step):
         Ts, x, gw, ex = steps[step - 1]
@@ -124,8 +134,7 @@ def main():
     def combine(step):
         Ts = steps[step - 1][0]
         first, cnt = plan.shard(Ts, rank)
-        outs[step] = torch.empty(cnt, d_h, dtype=torch.bfloat16, device=dev)
-        box.combine(outs[step], Ts, step, stream)
+        box.combine(outs[step], Ts, step, cstream)
 
     # one stream per rank; a colocated rank interleaves its roles in the same
     # order as the split box's ranks would (dispatch before MoE before combine).
@@ -144,7 +153,7 @@ def main():
                 dispatch(step)
             phase_end()
             if moe:
-                box.moe_step(steps[step - 1][0], step, stream)
+                box.moe_step(steps[step - 1][0], step, mstream)
             phase_end()
             if att:
                 combine(step)
@@ -158,7 +167,7 @@ def main():
                 dispatch(step + 1)
             phase_end()
             if moe:
-                box.moe_step(steps[step - 1][0], step, stream)
+                box.moe_step(steps[step - 1][0], step, mstream)
             phase_end()
             if att:
                 combine(step)
@@ -202,7 +211,7 @@ def main():
     except Exception as ex_:  # noqa: BLE001
         result["check"] = str(ex_)
     os.makedirs(args.out, exist_ok=True)
-    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}{args.combine}_{args.inflight}{'s' if args.shared else ''}{'x' if args.shared_split else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}_rank{rank}.json"), "w") as f:
+    with open(os.path.join(args.out, f"dist_{args.attn}a{args.moe}m_{args.transport}{args.combine}_{args.inflight}{'s' if args.shared else ''}{'x' if args.shared_split else ''}{'g' if args.gate else ''}{'c' if args.colocated else ''}{'t' if args.split_streams else ''}_rank{rank}.json"), "w") as f:
         json.dump(result, f)
     dist.barrier()
     dist.destroy_process_group()

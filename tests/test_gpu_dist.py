@@ -121,6 +121,39 @@ def test_moe_only_colocated_box(n, transport):
             assert s_["bad"] == 0, s_
 
 
+@pytest.mark.parametrize("n,transport,colocated", [(2, "routed", True), (4, "routed", True),
+                                                  (4, "p2p", True), (4, "ce", True),
+                                                  (4, "nvls", True), (4, "routed", False),
+                                                  (4, "p2p", False)])
+def test_box_split_streams(n, transport, colocated):
+    """Dispatch, MoE step and combine each on a stream of their own (as
+    bench.py runs the box), two steps in flight, five steps: the three epoch
+    slots are kept safe by the library's events and flags, not stream order.
+    Every shard vs the fp32 oracle."""
+    if gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = tempfile.mkdtemp()
+    roles = ["--attn", str(n), "--moe", str(n), "--colocated"] if colocated else \
+        ["--attn", "1", "--moe", str(n - 1)]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29600 + 10 * n + {"routed": 0, "p2p": 1, "ce": 2, "nvls": 3}[transport] +
+               (5 if colocated else 0)),
+           os.path.join(ROOT, "tests", "dist_worker.py"), *roles, "--out", out,
+           "--transport", transport, "--inflight", "2", "--steps", "7", "--split-streams"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
+    assert len(res) == n
+    for r in res:
+        assert not r["timed_out"], r
+        assert r["check"] == "ok", r
+        if r["role"] in ("both", "attention"):
+            assert len(r["steps"]) == 7
+            for s_ in r["steps"]:
+                assert s_["bad"] == 0, s_
+
+
 @pytest.mark.parametrize("box,transport", [("moe-only", "routed"), ("moe-only", "ce"),
                                            ("2a6e", "routed"), ("2a6e", "p2p")])
 def test_box_8_ranks_oversubscribed(box, transport):
