@@ -605,7 +605,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def box_trace(box, run_steps, s, s_moe, att, moe, rank, epoch, n=30):
+def box_trace(box, run_steps, s, s_moe, s_comb, att, moe, rank, epoch, n=30):
     """JANUS_BOX_TRACE=1: the pipelined box loop again with CUDA events around
     every enqueued call (dispatch / combine on the attention stream, the MoE
     step on its own), written to gpurun_out/boxtrace_rank{r}.json — when each
@@ -625,7 +625,7 @@ def box_trace(box, run_steps, s, s_moe, att, moe, rank, epoch, n=30):
         return f
     box.dispatch = wrap("dispatch", orig[0], s)
     box.moe_step = wrap("moe", orig[1], s_moe)
-    box.combine = wrap("combine", orig[2], s)
+    box.combine = wrap("combine", orig[2], s_comb)
     torch.cuda.synchronize()
     dist.barrier()
     base = torch.cuda.Event(enable_timing=True)
@@ -751,7 +751,7 @@ def run_box(args):
         lib.janus_profile(layer.ctx, 0)
         ffn = [a_.value / max(c_.value, 1), b_.value / max(c_.value, 1), 1.0]
     if os.environ.get("JANUS_BOX_TRACE"):  # diagnostics: per-call events of the pipelined loop
-        box_trace(box, run_steps, s, s_moe, att, moe, rank, epoch)
+        box_trace(box, run_steps, s, s_moe, s_comb, att, moe, rank, epoch)
     # dispatch kernel alone (attention ranks): events around the dispatch only,
     # over extra steps after the timed region
     # each phase alone, one step in flight: attention dispatch; MoE step (from
