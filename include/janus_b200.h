@@ -238,7 +238,11 @@ janus_status janus_xfer_handle(const janus_ctx *ctx, uint8_t *handle /* 64 bytes
 janus_status janus_xfer_connect(janus_ctx *ctx, const uint8_t *handles /* world x 64, by rank */);
 /* device, attention rank a: push this rank's shard (janus_shard_tokens of the
  * step's num_tokens) — rows x [T_a][d_h] bf16, experts / gate_w [T_a*k] — into
- * every MoE rank, then publish `epoch` (> 0, increasing per step).  With both
+ * every MoE rank, then publish `epoch` (> 0, increasing per step).  Three
+ * epoch slots: call janus_attn_combine_async(epoch - 3) (and, colocated, the
+ * MoE step of epoch - 3) before this; the dispatch then waits on the device
+ * until that step is done everywhere, so dispatch and combine may use
+ * different streams.  With both
  * routing pointers NULL only the rows move: the MoE ranks gate themselves
  * (janus_moe_set_router on their contexts; Janus gates on the MoE side,
  * PAPER.md:671-678). */
