@@ -697,7 +697,9 @@ static int push_blocks() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return 4 * sms;
+  // JANUS_PUSH_BLOCKS: tuning override of the measured default
+  static const int over = getenv("JANUS_PUSH_BLOCKS") ? atoi(getenv("JANUS_PUSH_BLOCKS")) : 0;
+  return over > 0 ? over : 4 * sms;
 }
 
 static janus_status layer_run(janus_ctx *ctx, const void *d_x, const int32_t *d_experts,

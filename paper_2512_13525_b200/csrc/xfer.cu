@@ -385,7 +385,9 @@ int side_grid(long long work) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return std::min(grid_for(work), std::max(8, sms / 3));
+  // JANUS_DISPATCH_CTAS: tuning override of the measured default (SMs / 3)
+  static const int over = getenv("JANUS_DISPATCH_CTAS") ? atoi(getenv("JANUS_DISPATCH_CTAS")) : 0;
+  return std::min(grid_for(work), over > 0 ? over : std::max(8, sms / 3));
 }
 
 
