@@ -578,7 +578,10 @@ cudaError_t launch_reduce_partials(const XferState &x, void *d_out, long long Ta
                                    unsigned long long epoch, cudaStream_t s) {
   if (Ta == 0) return cudaSuccess;
   const unsigned char *base = static_cast<const unsigned char *>(x.local);
-  reduce_partials_kernel<<<grid_for(Ta * (x.d_h / 8)), 256, 0, s>>>(
+  // JANUS_REDUCE_CTAS: tuning override of the grid (default: the work, <= 8 x SMs)
+  static const int over = getenv("JANUS_REDUCE_CTAS") ? atoi(getenv("JANUS_REDUCE_CTAS")) : 0;
+  const int grid = over > 0 ? std::min(over, grid_for(Ta * (x.d_h / 8))) : grid_for(Ta * (x.d_h / 8));
+  reduce_partials_kernel<<<grid, 256, 0, s>>>(
       reinterpret_cast<const __nv_bfloat16 *>(base + x.L.part_off +
                                                xfer_slot(epoch) * x.L.slot_stride),
       x.M, Ta, x.L.ta_max, x.d_h,
