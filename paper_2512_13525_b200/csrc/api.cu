@@ -1117,7 +1117,8 @@ janus_status janus_xfer_connect_local(janus_ctx *ctx, janus_ctx *const *peers) {
 // wait kernel spinning on other GPUs only).  Once per epoch.
 static janus_status slot_free_wait(janus_ctx *ctx, uint64_t epoch, cudaStream_t s) {
   janus::XferState &x = ctx->xfer;
-  if (epoch <= (uint64_t)janus::kXferSlots || x.slot_epoch == epoch) return JANUS_OK;
+  if (epoch <= (uint64_t)janus::kXferSlots || (x.slot_epoch == epoch && x.slot_stream == s))
+    return JANUS_OK;
   const size_t sl = janus::xfer_slot(epoch);
   if (x.comb_done[sl]) CK(cudaStreamWaitEvent(s, x.comb_done[sl], 0));
   const cudaEvent_t own = x.own_sig[sl];
@@ -1126,6 +1127,7 @@ static janus_status slot_free_wait(janus_ctx *ctx, uint64_t epoch, cudaStream_t 
   if (e != cudaSuccess) return cuda_fail(ctx, e, "wait_flags_kernel");
   ctx->launches += 1;
   x.slot_epoch = epoch;
+  x.slot_stream = s;
   return JANUS_OK;
 }
 

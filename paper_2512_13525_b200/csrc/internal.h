@@ -200,6 +200,7 @@ struct XferState {
   int transport = kXferP2P;
   unsigned long long routed_epoch = 0;  // routed: routing of this epoch already pushed
   unsigned long long slot_epoch = 0;    // the slot-free wait of this epoch already enqueued
+  void *slot_stream = nullptr;          // ... on this stream
   // routed transport, attention side: the step's schedule (K1 over every
   // shard's routing) and each owned token's destination-instance mask per
   // epoch slot ([kXferSlots][ta_max])
