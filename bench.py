@@ -717,13 +717,19 @@ def run_box(args):
     # attention rank dispatches step i+1 before it combines step i, so the MoE
     # GPUs find step i+1's rows already delivered when they finish step i.
     # (a colocated rank interleaves its two roles in that order on one stream)
+    # dispatches run `ahead` steps ahead of the MoE step (the library's three
+    # epoch slots allow up to 2: combine(e-3) is enqueued before dispatch(e))
+    ahead = int(os.environ.get("JANUS_BOX_AHEAD", "1"))
+
     def run_steps(n, i0=0):
         e0_ = epoch[0]
         if att:
-            box.dispatch(xs, exs[i0 % N_BATCHES], gws[0], T, e0_ + 1, stream)
+            for j in range(min(ahead, n)):
+                box.dispatch(xs, exs[(i0 + j) % N_BATCHES], gws[0], T, e0_ + j + 1, stream)
         for j in range(n):
-            if att and j + 1 < n:
-                box.dispatch(xs, exs[(i0 + j + 1) % N_BATCHES], gws[0], T, e0_ + j + 2, stream)
+            if att and j + ahead < n:
+                box.dispatch(xs, exs[(i0 + j + ahead) % N_BATCHES], gws[0], T, e0_ + j + ahead + 1,
+                             stream)
             if moe:
                 box.moe_step(T, e0_ + j + 1, stream_moe)
             if att:
