@@ -1,5 +1,6 @@
 #!/bin/bash
 # box: MoE stream priority (highest vs default), N = 4 and 2, interleaved
+# (JANUS_MOE_PRIO was a temporary bench.py knob: s_moe = torch.cuda.Stream(dev, priority=-1); removed after this measurement)
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 O=gpurun_out/prio; mkdir -p $O
 run() {
