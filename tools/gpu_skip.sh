@@ -1,3 +1,4 @@
+# (a measurement with an experiment build, exp_libs/skip.so, whose push kernel returned at once when JANUS_SKIP_PUSH=1; that build and knob are not in the tree)
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 cp exp_libs/skip.so paper_2512_13525_b200/libjanus_b200.so
 for sp in "" 1; do
