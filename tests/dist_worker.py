@@ -47,8 +47,8 @@ def main():
                     help="MoE-only box: every rank owns a shard and is an MoE instance")
     ap.add_argument("--gate", action="store_true",
                     help="MoE-side gating: dispatch rows only, MoE ranks run the router")
-    ap.add_argument("--inflight", type=int, default=1, choices=[1, 2],
-                    help="2: dispatch step s+1 before combining step s (double-buffered slots)")
+    ap.add_argument("--inflight", type=int, default=1, choices=[1, 2, 3],
+                    help="2 / 3: dispatch step s+1 / s+2 before combining step s (three epoch slots)")
     ap.add_argument("--split-streams", action="store_true",
                     help="combines on a stream of their own (the slots kept safe by the library)")
     args = ap.parse_args()
@@ -158,13 +158,15 @@ def main():
             if att:
                 combine(step)
             torch.cuda.synchronize()
-    else:
+    else:  # dispatches inflight - 1 steps ahead of the MoE step
+        ahead = args.inflight - 1
         if att:
-            dispatch(1)
+            for j in range(1, min(ahead, args.steps) + 1):
+                dispatch(j)
         phase_end()
         for step in range(1, args.steps + 1):
-            if att and step < args.steps:
-                dispatch(step + 1)
+            if att and step + ahead <= args.steps:
+                dispatch(step + ahead)
             phase_end()
             if moe:
                 box.moe_step(steps[step - 1][0], step, mstream)

@@ -121,15 +121,16 @@ def test_moe_only_colocated_box(n, transport):
             assert s_["bad"] == 0, s_
 
 
-@pytest.mark.parametrize("n,transport,colocated", [(2, "routed", True), (4, "routed", True),
-                                                  (4, "p2p", True), (4, "ce", True),
-                                                  (4, "nvls", True), (4, "routed", False),
-                                                  (4, "p2p", False)])
-def test_box_split_streams(n, transport, colocated):
+@pytest.mark.parametrize("n,transport,colocated,inflight", [
+    (2, "routed", True, 2), (4, "routed", True, 2), (4, "p2p", True, 2), (4, "ce", True, 2),
+    (4, "nvls", True, 2), (4, "routed", False, 2), (4, "p2p", False, 2),
+    (4, "routed", True, 3), (4, "p2p", False, 3)])
+def test_box_split_streams(n, transport, colocated, inflight):
     """Dispatch, MoE step and combine each on a stream of their own (as
-    bench.py runs the box), two steps in flight, five steps: the three epoch
-    slots are kept safe by the library's events and flags, not stream order.
-    Every shard vs the fp32 oracle."""
+    bench.py runs the box), two or three steps in flight (dispatches one or
+    two steps ahead), seven steps: the three epoch slots are kept safe by the
+    library's events and flags, not stream order.  Every shard vs the fp32
+    oracle."""
     if gpus() < n:
         pytest.skip(f"needs {n} GPUs")
     out = tempfile.mkdtemp()
@@ -138,9 +139,10 @@ def test_box_split_streams(n, transport, colocated):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
            str(29600 + 10 * n + {"routed": 0, "p2p": 1, "ce": 2, "nvls": 3}[transport] +
-               (5 if colocated else 0)),
+               (5 if colocated else 0) + 50 * (inflight - 2)),
            os.path.join(ROOT, "tests", "dist_worker.py"), *roles, "--out", out,
-           "--transport", transport, "--inflight", "2", "--steps", "7", "--split-streams"]
+           "--transport", transport, "--inflight", str(inflight), "--steps", "7",
+           "--split-streams"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     res = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(out, "*.json")))]
